@@ -1,0 +1,384 @@
+"""HATA decode hot path benchmark (driver contract).
+
+python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg4] [--impl reference]
+
+A step = one decode step of one attention layer over one batch: hata_append
+(new k/v + key code) followed by hata_decode_topk_attn (q-hash, Hamming
+score, exact top-k, gather-attention, combine) -- every §8(a) decode row.
+Inputs are synthetic (synth.make_case recipe) and resident in HBM; steps
+rotate over 16 distinct cache sets so that consecutive steps never hit in
+the 126 MB L2.  N > 1 (torchrun): the context is sequence-sharded across the
+ranks with the NCCL global top-k merge and split-softmax combine (strong
+scaling).  Rank 0 prints one JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+import synth  # noqa: E402
+
+METRIC = "decode attention µs/step & tokens/s at 32K/128K ctx; HBM GB/s vs roofline"
+N_SETS = 16
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            mp = json.load(f)
+        return float(mp["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def algorithmic_bytes(sh, N=None, k=None):
+    """codes + k' selected K/V rows + q (north_star roofline definition)."""
+    N = sh.N if N is None else N
+    k = sh.k if k is None else k
+    eb = 2 if sh.dtype == "bf16" else 4
+    kp = min(k, N)
+    return sh.B * sh.Hkv * N * sh.rbits // 8 + sh.B * sh.Hkv * kp * 2 * sh.d * eb + sh.B * sh.Hq * sh.d * eb
+
+
+class ClockSampler:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([c.strip() for c in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            for nm, v in zip(names, r[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.rows)}
+
+
+# ---------------------------------------------------------------------------
+# single-GPU step
+# ---------------------------------------------------------------------------
+class Step:
+    """Device-resident inputs of one layer step + preallocated outputs."""
+
+    def __init__(self, sh, seed, device):
+        import paper_2506_02572_b200 as H
+        self.H = H
+        c = synth.make_case(sh, seed, device=device, variant="planted")
+        # planted rows (cheap on device): sinks + recent window get the group query direction
+        self.sh = sh
+        self.q, self.K, self.V, self.W = c["q"], c["K"], c["V"], c["W"]
+        self.kn, self.vn = c["k_new"], c["v_new"]
+        self.pos = c["n_before"]
+        self.n = self.pos + 1
+        B, Hkv, cap, d = self.K.shape
+        self.codes = torch.zeros(B, Hkv, cap, sh.rbits // 32, dtype=torch.int32, device=device)
+        H.hash_keys(self.K, self.W, self.codes, 0, sh.N - 1)
+        self.out = torch.empty(B, sh.Hq, d, dtype=torch.float32, device=device)
+        ws = H.decode_workspace_size(B, sh.Hq, Hkv, d, sh.rbits, sh.N, sh.k, self.K.dtype)
+        self.ws = torch.empty(max(ws, 1), dtype=torch.uint8, device=device)
+
+    def append(self):
+        self.H.append(self.kn, self.vn, self.W, self.K, self.V, self.codes, self.pos)
+
+    def decode(self):
+        self.H.decode_topk_attn(self.q, self.K, self.V, self.codes, self.W, self.n, self.sh.k, n_max=self.sh.N,
+                                out=self.out, workspace=self.ws)
+
+    def run(self):
+        self.append()
+        self.decode()
+
+
+def _graph(fn):
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        fn()  # warm / plan outside capture
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        fn()
+    return g
+
+
+def time_graphs(graphs, steps):
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record()
+    for i in range(steps):
+        graphs[i % len(graphs)].replay()
+    e1.record()
+    e1.synchronize()
+    return e0.elapsed_time(e1) / 1e3  # s
+
+
+def bench_single(sh, steps, warmup, device, n_sets=N_SETS):
+    sets = [Step(sh, 1000 + i, device) for i in range(n_sets)]
+    step_graphs = [_graph(s.run) for s in sets]
+    dec_graphs = [_graph(s.decode) for s in sets]
+    for i in range(max(warmup, 3)):
+        step_graphs[i % n_sets].replay()
+    torch.cuda.synchronize()
+    with ClockSampler(torch.cuda.current_device()) as cs:
+        t_step = time_graphs(step_graphs, steps)
+        t_dec = time_graphs(dec_graphs, steps)   # dominant kernel alone, same rotation
+    return dict(t_step=t_step, t_dec=t_dec, clocks=cs.summary(), sets=sets)
+
+
+def bench_e2e(sh, steps, device):
+    """Same metric through the public API with HOST buffers: per step, pinned
+    q/k_new/v_new go H2D, append + decode run, the output comes back D2H."""
+    s = Step(sh, 77, device)
+    hq = s.q.cpu().pin_memory()
+    hk = s.kn.cpu().pin_memory()
+    hv = s.vn.cpu().pin_memory()
+    ho = torch.empty(s.out.shape, dtype=s.out.dtype).pin_memory()
+    for _ in range(3):
+        s.q.copy_(hq, non_blocking=True); s.kn.copy_(hk, non_blocking=True); s.vn.copy_(hv, non_blocking=True)
+        s.run(); ho.copy_(s.out, non_blocking=True); torch.cuda.current_stream().synchronize()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        s.q.copy_(hq, non_blocking=True)
+        s.kn.copy_(hk, non_blocking=True)
+        s.vn.copy_(hv, non_blocking=True)
+        s.run()
+        ho.copy_(s.out, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+    dt = time.perf_counter() - t0
+    h2d = hq.numel() * hq.element_size() + hk.numel() * hk.element_size() + hv.numel() * hv.element_size()
+    d2h = ho.numel() * ho.element_size()
+    return dict(value=sh.B * steps / dt, unit="tokens/s", us_per_step=dt / steps * 1e6,
+                h2d_bytes_per_step=h2d, d2h_bytes_per_step=d2h)
+
+
+def dense_baseline(st, steps):
+    """Full-attention decode over the same cache (context, north_star)."""
+    q = st.q.view(st.sh.B, st.sh.Hq, 1, st.sh.d)
+    K, V = st.K, st.V
+    try:
+        from flash_attn import flash_attn_with_kvcache
+        qf = st.q.view(st.sh.B, 1, st.sh.Hq, st.sh.d)
+        kc, vc = K.transpose(1, 2), V.transpose(1, 2)
+        cs = st.n.to(torch.int32)
+        fn = lambda: flash_attn_with_kvcache(qf, kc, vc, cache_seqlens=cs)  # noqa: E731
+        fn()
+        impl = "flash_attn.flash_attn_with_kvcache"
+    except Exception:
+        fn = lambda: torch.nn.functional.scaled_dot_product_attention(q, K, V, enable_gqa=True)  # noqa: E731
+        impl = "torch SDPA (enable_gqa)"
+    fn()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        fn()
+    e1.record()
+    e1.synchronize()
+    return {"impl": impl, "us_per_step": e0.elapsed_time(e1) / steps * 1e3,
+            "note": "same resident cache every step (L2-warm upper bound for dense)"}
+
+
+def cpu_oracle_baseline(sh, budget_s=12.0, heads=None):
+    """The oracle as it stands on a bounded sample: one full decode step of one
+    (b, KV head) group of this workload (append + q-hash + score + top-k +
+    attention for its G query heads), repeated for ~budget_s seconds."""
+    import numpy as np
+    try:
+        from threadpoolctl import threadpool_limits
+        lim = threadpool_limits(1)
+    except Exception:
+        lim = None
+    import oracle.hata_oracle as O
+    import dataclasses
+    one = dataclasses.replace(sh, B=1, Hq=sh.G, Hkv=1)
+    c = synth.make_case(one, 4242, device="cpu", variant="plain")
+    K = c["K"].float().numpy(); V = c["V"].float().numpy(); W = c["W"].float().numpy()
+    q = c["q"].float().numpy(); kn = c["k_new"].float().numpy(); vn = c["v_new"].float().numpy()
+    codes, _ = O.hash_keys(K, W)
+    nb = c["n_before"].numpy()
+    reps, t0 = 0, time.perf_counter()
+    while True:
+        O.decode_step(q, kn, vn, K, V, codes, W, nb, sh.k)
+        reps += 1
+        if time.perf_counter() - t0 > budget_s:
+            break
+    dt = (time.perf_counter() - t0) / reps
+    if lim is not None:
+        lim.unregister() if hasattr(lim, "unregister") else None
+    groups = sh.B * sh.Hkv
+    per_step = dt * groups
+    return {"value": sh.B / per_step, "unit": "tokens/s", "cores": 1, "kind": "oracle",
+            "sample": f"{reps} oracle decode steps of one (b, KV head) group ({sh.G} q heads, N={sh.N}, "
+                      f"k={sh.k}), fp64 numpy, 1 thread; step time = group time x {groups} groups",
+            "s_per_group_step": dt, "cpu": _cpu_name()}
+
+
+def _cpu_name():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def run_reference(args, sh, rank):
+    """--impl reference: the CPU oracle as it stands (this tier's reference arm)."""
+    if rank != 0:
+        return
+    import oracle.hata_oracle as O
+    import dataclasses
+    one = dataclasses.replace(sh, B=1, Hq=sh.G, Hkv=1)
+    c = synth.make_case(one, 4242, device="cpu", variant="plain")
+    K = c["K"].float().numpy(); V = c["V"].float().numpy(); W = c["W"].float().numpy()
+    q = c["q"].float().numpy(); kn = c["k_new"].float().numpy(); vn = c["v_new"].float().numpy()
+    codes, _ = O.hash_keys(K, W)
+    nb = c["n_before"].numpy()
+    for _ in range(args.warmup):
+        O.decode_step(q, kn, vn, K, V, codes, W, nb, sh.k)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        O.decode_step(q, kn, vn, K, V, codes, W, nb, sh.k)
+    dt = (time.perf_counter() - t0) / args.steps
+    groups = sh.B * sh.Hkv
+    value = sh.B / (dt * groups)
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * groups * 1e3,
+            "higher_is_better": True, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": sh.name + ": " + sh.note, "B": sh.B, "Hq": sh.Hq, "Hkv": sh.Hkv, "d": sh.d,
+                       "rbits": sh.rbits, "N": sh.N, "k": sh.k},
+            "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": 1, "kind": "oracle",
+                             "sample": f"each step = one (b, KV head) group of the workload "
+                                       f"(x{groups} to a full step)"},
+            "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--config", default="cfg4")
+    ap.add_argument("--impl", default="hata", choices=["hata", "reference"])
+    ap.add_argument("--no-cpu", action="store_true", help="skip the oracle cpu_baseline leg")
+    ap.add_argument("--no-secondary", action="store_true")
+    args = ap.parse_args()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    sh = synth.CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, sh, rank)
+        return
+    if world > 1:
+        from paper_2506_02572_b200 import seqshard_bench
+        seqshard_bench.main(args, sh, rank, world)
+        return
+    device = torch.device("cuda", 0)
+    torch.cuda.set_device(device)
+    peak, peak_src = _peaks()
+    r = bench_single(sh, args.steps, args.warmup, device)
+    bytes_step = algorithmic_bytes(sh)
+    us_step = r["t_step"] / args.steps * 1e6
+    us_dec = r["t_dec"] / args.steps * 1e6
+    achieved = bytes_step / (us_dec * 1e-6) / 1e9
+    H = r["sets"][0].H
+    C = H.decode_cluster_size(sh.B, sh.Hq, sh.Hkv, sh.d, sh.rbits, sh.N, sh.k, r["sets"][0].K.dtype)
+    line = {
+        "metric": METRIC, "value": sh.B * args.steps / r["t_step"], "unit": "tokens/s (one attention layer)",
+        "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": us_step / 1e3,
+        "us_per_step": us_step, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": sh.dtype, "data": "synthetic (synth.make_case, seeds 1000-1015)",
+        "config": {"workload": f"{sh.name}: {sh.note}", "B": sh.B, "Hq": sh.Hq, "Hkv": sh.Hkv, "d": sh.d,
+                   "rbits": sh.rbits, "N": sh.N, "k": sh.k, "cluster": C,
+                   "l2": f"rotating {N_SETS} distinct cache sets ({N_SETS} x {bytes_step / 1e6:.1f} MB step bytes "
+                         f"> 126 MB L2)", "parallelism": "single GPU"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": None, "kernel": "hata_decode_kernel", "algorithmic_bytes_per_launch": bytes_step,
+                     "us_per_launch": us_dec, "peak_source": peak_src,
+                     "frac_vs_8TBs": achieved / 8000.0},
+        "clocks": r["clocks"],
+        "gpu_launches": 2 * args.steps,
+    }
+    del r
+    e2e = bench_e2e(sh, min(args.steps, 200), device)
+    line["e2e"] = e2e
+    if not args.no_secondary:
+        sec = {}
+        for nm in ("cfg2",):
+            if nm == sh.name:
+                continue
+            s2 = synth.CONFIGS[nm]
+            r2 = bench_single(s2, args.steps, args.warmup, device, n_sets=N_SETS)
+            b2 = algorithmic_bytes(s2)
+            u2 = r2["t_step"] / args.steps * 1e6
+            ud = r2["t_dec"] / args.steps * 1e6
+            sec[nm] = {"workload": s2.note, "us_per_step": u2, "tokens_per_s": s2.B / (u2 * 1e-6),
+                       "decode_us": ud, "achieved_GBps": b2 / (ud * 1e-6) / 1e9,
+                       "frac": b2 / (ud * 1e-6) / 1e9 / peak}
+            st = r2["sets"][0]
+            sec[nm]["dense_baseline"] = dense_baseline(st, 50)
+            del r2
+        line["secondary"] = sec
+    st = Step(sh, 1000, device)
+    line["dense_baseline"] = dense_baseline(st, 50)
+    line["dense_baseline"]["speedup_vs_dense"] = line["dense_baseline"]["us_per_step"] / us_dec
+    del st
+    if not args.no_cpu:
+        line["cpu_baseline"] = cpu_oracle_baseline(sh)
+    print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,197 @@
+/*
+ * libhata -- C ABI of the B200 (sm_100a) HATA decode hot path.
+ *
+ * HATA = Hash-Aware Top-k Attention (arXiv 2506.02572).  Citations: "P:n" is
+ * line n of the paper text (/root/reference/PAPER.md, LaTeX source), with the
+ * algorithm / section it falls in.  Readings R1..R20 of places where the paper
+ * is silent are listed in DESIGN.md.
+ *
+ * CONVENTIONS (all entry points)
+ *  - Every pointer is caller-owned DEVICE memory unless stated otherwise; the
+ *    library never allocates, frees or synchronises.  Work is enqueued on
+ *    `stream` (a cudaStream_t; NULL = legacy default stream) and is
+ *    asynchronous: outputs are valid once the stream reaches that point.
+ *  - Argument validation is synchronous and happens before any launch; on a
+ *    validation failure nothing is enqueued and outputs are untouched.
+ *  - Launch failures return HATA_ERR_CUDA; hata_last_error() has the text.
+ *    Faults inside a kernel surface at the caller's next synchronising call.
+ *  - Nothing throws across this boundary.
+ *  - Tensors:
+ *      KV cache   K, V   [B, H_kv, cap, d]  element strides {sb, sh, st},
+ *                        d contiguous (stride 1); bf16 or fp32.
+ *      code cache codes  [B, H_kv, cap, rbits/32] uint32 word strides
+ *                        {sb, sh, st}; st must equal rbits/32 (rows packed),
+ *                        rows 16-byte aligned when rbits >= 128.
+ *      hash weight W     [H_kv, d, rbits] contiguous, same dtype as K
+ *                        (one W_H per KV head, shared by its G query heads; R4).
+ *      queries    q      [B, H_q, d] contiguous; query head h reads KV head
+ *                        h / G with G = H_q / H_kv (R5).
+ *  - Codes: bit b of a row is 1 iff (x . W[:, b]) >= 0 (sign(0) -> +1, R6),
+ *    stored LSB-first in word b / 32 (R7).  Projections accumulate in fp32.
+ *  - Supported: d == 128; rbits in {32, 64, 128, 256}; G = H_q/H_kv <= 8;
+ *    dtype bf16 or fp32.  Other shapes return HATA_ERR_UNSUPPORTED.
+ *  - Thread safety: calls may be made from any host thread; one writer per
+ *    cache (the caller orders append before decode on the stream).
+ */
+#ifndef HATA_H_
+#define HATA_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  HATA_OK = 0,
+  HATA_ERR_INVALID_ARG = 1, /* bad shape/pointer/stride (e.g. rbits % 32, H_q % H_kv, k < 1) */
+  HATA_ERR_UNSUPPORTED = 2, /* valid but not compiled for this shape/dtype */
+  HATA_ERR_CAPACITY = 3,    /* host-checked capacity violation (n > cap) */
+  HATA_ERR_WORKSPACE = 4,   /* workspace missing or smaller than hata_decode_workspace_size() */
+  HATA_ERR_CUDA = 5         /* a CUDA launch failed; see hata_last_error() */
+} hata_status;
+
+typedef enum { HATA_F32 = 0, HATA_BF16 = 1 } hata_dtype;
+
+/* Element (or word) strides of a [B, H_kv, cap, x] tensor; x is contiguous. */
+typedef struct {
+  int64_t sb, sh, st;
+} hata_strides;
+
+typedef struct CUstream_st* hata_stream_t; /* == cudaStream_t */
+
+/* ------------------------------------------------------------------------
+ * hata_hash_keys -- HashEncode every cached key of a prefilled cache.
+ * PAPER: Alg. 1 "HATA Prefill Stage" lines 2-5 with Alg. 2
+ * HashEncode: K_H <- BitPack(Sign(MatMul(K, W_H))); fill the
+ * key code cache.
+ *   K       [B, H_kv, cap, d] (strides ks), rows [t0, t0 + n) are hashed.
+ *   W       [H_kv, d, rbits].
+ *   codes   output rows [t0, t0 + n) of [B, H_kv, cap, rbits/32] (strides cs).
+ * bf16 inputs run on the tcgen05 tensor cores (fp32 accumulation in TMEM,
+ * sign-pack epilogue); fp32 inputs run on CUDA cores (fp32 FMA).
+ * Errors: INVALID_ARG (null pointers, n < 0, rbits % 32, strides),
+ *         UNSUPPORTED (d, rbits, dtype), CUDA.
+ * ------------------------------------------------------------------------ */
+hata_status hata_hash_keys(const void* K, hata_strides ks, hata_dtype dt, const void* W, int B, int H_kv, int d,
+                           int rbits, int64_t t0, int64_t n, uint32_t* codes, hata_strides cs,
+                           hata_stream_t stream);
+
+/* ------------------------------------------------------------------------
+ * hata_append -- decode-time cache update for the new token.
+ * PAPER: Alg. 3 "HATA Decode Stage" lines 2-9: K^cache <- [K^cache; K],
+ * V^cache <- [V^cache; V], K_H <- HashEncode(K), K_H^cache <- [K_H^cache; K_H];
+ * fused into one kernel as in §4 "Kernel fusion for hash encoding".
+ *   k_new, v_new [B, H_kv, d] contiguous, dtype dt.
+ *   K, V, codes  caches (strides kvs / cs) written at row pos[b].
+ *   pos          DEVICE int64 [B]: row to write (= tokens cached before this step).
+ *   cap          rows allocated per (b, g).  A pos[b] outside [0, cap) is skipped
+ *                on the device (cannot be validated synchronously).
+ * Errors: INVALID_ARG, UNSUPPORTED, CUDA.
+ * ------------------------------------------------------------------------ */
+hata_status hata_append(const void* k_new, const void* v_new, hata_dtype dt, const void* W, void* K, void* V,
+                        hata_strides kvs, uint32_t* codes, hata_strides cs, const int64_t* pos, int64_t cap, int B,
+                        int H_kv, int d, int rbits, hata_stream_t stream);
+
+/* ------------------------------------------------------------------------
+ * hata_decode_topk_attn -- one decode step over caches that already hold the
+ * new token (call hata_append first on the same stream).
+ * PAPER: Alg. 3 lines 6 and 10-17, P:254-255:
+ *   Q_H  <- HashEncode(q) per query head (W of its KV head, R4/R5);
+ *   D[t] <- sum over the G query heads of the group of bitcount(xor(Q_H, K_H^cache[t]))
+ *           for t < n[b], including the appended token (R3, R11);
+ *   Idx  <- the k' = min(k, n[b]) tokens of smallest D (= largest similarity
+ *           S = G*rbits - 2D; R1, R2), ties to the LOWEST index (R8),
+ *           reported in ascending order (R9);
+ *   out[b, h] <- softmax(scale * q_h . K[Idx]^T) V[Idx]  (Eq. 1, Eq. 2),
+ *           gather fused into the attention.
+ * Arguments:
+ *   q          [B, H_q, d] dtype dt.
+ *   K, V       caches (strides kvs), dtype dt.  codes (strides cs).  W as above.
+ *   n          DEVICE int64 [B]: tokens per sequence incl. the appended one.
+ *   n_max      host upper bound on n[b] (sizes the launch and the workspace).
+ *   k          token budget per (b, KV head), >= 1; k > n[b] clamps (R10).
+ *   scale      softmax scale; 0 selects 1/sqrt(d) (R12).
+ *   out        [B, H_q, d] dtype out_dt (fp32 recommended for parity, R14).
+ *   out_idx    optional [B, H_kv, k] int32: selected token indices ascending,
+ *              -1 padding beyond k'.
+ *   out_score  optional [B, H_kv, k] int32: S = G*rbits - 2D of those tokens.
+ *   out_qcodes optional [B, H_q, rbits/32] uint32: the query codes used.
+ *   workspace  device scratch of >= hata_decode_workspace_size(...) bytes
+ *              (may be NULL when that size is 0).
+ * One kernel launch: one thread-block cluster per (b, KV head).
+ * Errors: INVALID_ARG (k < 1, H_q % H_kv, rbits % 32, n_max < 0, nulls),
+ *         UNSUPPORTED, WORKSPACE, CUDA.  n[b] == 0 yields zero output and
+ *         out_idx all -1.
+ * ------------------------------------------------------------------------ */
+hata_status hata_decode_topk_attn(const void* q, const void* K, const void* V, hata_strides kvs, hata_dtype dt,
+                                  const uint32_t* codes, hata_strides cs, const void* W, int B, int H_q, int H_kv,
+                                  int d, int rbits, const int64_t* n, int64_t n_max, int k, float scale, void* out,
+                                  hata_dtype out_dt, int32_t* out_idx, int32_t* out_score, uint32_t* out_qcodes,
+                                  void* workspace, size_t ws_bytes, hata_stream_t stream);
+
+/* Bytes of device workspace hata_decode_topk_attn needs for this shape
+ * (0 when everything fits on chip).  Host-only; never fails (0 on bad args). */
+size_t hata_decode_workspace_size(int B, int H_q, int H_kv, int d, int rbits, int64_t n_max, int k,
+                                  hata_dtype dt);
+
+/* Cluster size (CTAs per (b, KV head)) the decode launch will use; for tests/bench. */
+int hata_decode_cluster_size(int B, int H_q, int H_kv, int d, int rbits, int64_t n_max, int k, hata_dtype dt);
+
+/* ========================================================================
+ * Sequence-sharded decode (one rank owns a contiguous token range of every
+ * (b, KV head)).  The exchange steps between the
+ * phases are the caller's collectives (NCCL all-gather via torch.distributed).
+ * Because ranges are contiguous and ascending in rank, "lowest index wins"
+ * equals "lower rank first, then local order", so the merged selection is
+ * bit-identical to the unsharded one.
+ * ======================================================================== */
+
+/* Phase 1: local q-hash + score + local top-k' candidates.
+ *   K/V unused here; codes hold this rank's n_local[b] tokens, whose global
+ *   index is token_offset + local index.
+ *   cand_D    [B, H_kv, k] int32: aggregated distance D of each candidate
+ *             (INT32_MAX padding), ascending token order.
+ *   cand_idx  [B, H_kv, k] int32: GLOBAL token index (-1 padding).
+ * PAPER: Alg. 3 lines 6, 10-13 applied to the rank's slice. */
+hata_status hata_shard_candidates(const void* q, hata_dtype dt, const uint32_t* codes, hata_strides cs,
+                                  const void* W, int B, int H_q, int H_kv, int d, int rbits, const int64_t* n_local,
+                                  int64_t n_local_max, int64_t token_offset, int k, int32_t* cand_D,
+                                  int32_t* cand_idx, void* workspace, size_t ws_bytes, hata_stream_t stream);
+
+/* Phase 2: global merge.  all_D / all_idx are the P ranks' candidate lists
+ * gathered rank-major: [P, B, H_kv, k].  Selects the global k' = min(k, n_total[b])
+ * smallest (D, index) pairs (identical on every rank) and returns those that
+ * fall in [lo, hi) as LOCAL indices (global - lo), ascending, in own_idx
+ * [B, H_kv, k] (-1 padding) with counts own_cnt [B, H_kv].  Optionally the
+ * whole global selection (ascending) in sel_idx [B, H_kv, k] and its S values
+ * in sel_score.  n_total: DEVICE int64 [B]. */
+hata_status hata_shard_select(const int32_t* all_D, const int32_t* all_idx, int P, int B, int H_kv, int k, int G,
+                              int rbits, const int64_t* n_total, int64_t lo, int64_t hi, int32_t* own_idx,
+                              int32_t* own_cnt, int32_t* sel_idx, int32_t* sel_score, hata_stream_t stream);
+
+/* Phase 3: partial attention over own selected rows.
+ *   partial [B, H_q, d + 2] fp32: (m, l, acc[d]) with m = max logit,
+ *   l = sum exp(z - m), acc = sum exp(z - m) V  (flash-decoding partials). */
+hata_status hata_shard_partial_attn(const void* q, const void* K, const void* V, hata_strides kvs, hata_dtype dt,
+                                    const int32_t* own_idx, const int32_t* own_cnt, int B, int H_q, int H_kv, int d,
+                                    int k, float scale, float* partial, hata_stream_t stream);
+
+/* Phase 4: combine P partials gathered rank-major [P, B, H_q, d + 2] in rank
+ * order (deterministic): M = max m_r, L = sum l_r e^{m_r - M},
+ * out = sum acc_r e^{m_r - M} / L. */
+hata_status hata_shard_combine(const float* partials, int P, int B, int H_q, int d, void* out, hata_dtype out_dt,
+                               hata_stream_t stream);
+
+/* ------------------------------------------------------------------------ */
+const char* hata_status_string(hata_status s);
+/* Text of the last CUDA error seen by this host thread (empty if none). */
+const char* hata_last_error(void);
+/* Library version string. */
+const char* hata_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HATA_H_ */

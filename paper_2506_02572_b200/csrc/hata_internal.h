@@ -1,0 +1,67 @@
+// Internal (non-ABI) declarations shared by the libhata translation units.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stddef.h>
+
+namespace hata {
+
+struct AppendParams {
+  const void* k_new;   // [B, Hkv, d] contiguous
+  const void* v_new;
+  const void* Wh;      // [Hkv, d, rbits]
+  void* K;
+  void* V;
+  int64_t kv_sb, kv_sh, kv_st;
+  uint32_t* codes;
+  int64_t c_sb, c_sh;
+  const int64_t* pos;  // [B] device
+  int64_t cap;
+  int B, Hkv, d, rbits;
+};
+
+struct HashKeysParams {
+  const void* K;
+  int64_t kv_sb, kv_sh, kv_st;
+  const void* Wh;
+  uint32_t* codes;
+  int64_t c_sb, c_sh;
+  int64_t t0, n;       // rows [t0, t0 + n) of every (b, g)
+  int B, Hkv, d, rbits;
+};
+
+cudaError_t launch_append(const AppendParams& p, int is_bf16, cudaStream_t s);
+cudaError_t launch_hash_keys_simt(const HashKeysParams& p, int is_bf16, cudaStream_t s);
+// tcgen05 path (bf16, d == 128, rbits in {128, 256}); returns cudaErrorNotSupported otherwise.
+cudaError_t launch_hash_keys_tc(const HashKeysParams& p, cudaStream_t s);
+
+struct DecodePlan {
+  int C, chunk, rows_cap, nbins, GT;
+  bool gD, gsel;
+  size_t ws_D, ws_sel, ws_total;
+  int smem;
+};
+struct DecodeParams;
+DecodePlan plan_decode(int B, int Hq, int Hkv, int d, int rbits, int64_t n_max, int k, int elem_bytes);
+cudaError_t launch_decode(DecodeParams& p, const DecodePlan& plan, int is_bf16, cudaStream_t s);
+
+struct SelectParams {
+  const int32_t* all_D;    // [P, B, Hkv, k]
+  const int32_t* all_idx;  // [P, B, Hkv, k]
+  int P, B, Hkv, k, G, rbits;
+  const int64_t* n_total;  // [B]
+  int64_t lo, hi;
+  int32_t* own_idx;        // [B, Hkv, k]
+  int32_t* own_cnt;        // [B, Hkv]
+  int32_t* sel_idx;        // [B, Hkv, k] or null
+  int32_t* sel_score;      // [B, Hkv, k] or null
+};
+cudaError_t launch_shard_select(const SelectParams& p, cudaStream_t s);
+cudaError_t launch_shard_combine(const float* part, int P, int B, int Hq, int d, void* out, int out_bf16,
+                                 cudaStream_t s);
+struct PartialParams;
+cudaError_t launch_partial_attn(PartialParams& p, int GT, int is_bf16, cudaStream_t s);
+
+int device_sm_count();
+
+}  // namespace hata

@@ -51,7 +51,7 @@ __device__ __forceinline__ uint32_t score_naive(const uint32_t (&k)[W], const ui
 __device__ __forceinline__ uint32_t lop_mux(uint32_t k, uint32_t b, uint32_t a) {
   // k ? b : a  bitwise
   uint32_t r;
-  asm("lop3.b32 %0, %1, %2, %3, 0xE4;" : "=r"(r) : "r"(k), "r"(b), "r"(a));
+  asm("lop3.b32 %0, %1, %2, %3, 0xCA;" : "=r"(r) : "r"(k), "r"(b), "r"(a));
   return r;
 }
 __device__ __forceinline__ void fa(uint32_t a, uint32_t b, uint32_t c, uint32_t& s, uint32_t& cy) {

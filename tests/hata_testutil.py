@@ -1,0 +1,109 @@
+"""Test helpers: run the CUDA path through the C ABI and compare with the
+oracle following the north_star parity protocol.  (Tests only.)"""
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+import oracle.hata_oracle as O
+
+TOL = {"bf16": 2e-3, "f32": 1e-5}
+
+
+def to_np64(t: torch.Tensor) -> np.ndarray:
+    return t.detach().to("cpu", torch.float64).numpy()
+
+
+def codes_u32(t: torch.Tensor) -> np.ndarray:
+    return t.detach().cpu().numpy().view(np.uint32)
+
+
+def gpu_step(case: dict, k: int, n_override=None, out_dtype=torch.float32, device="cuda"):
+    """prefill-hash rows [0, N-1), append row n_before, decode; all via the C ABI."""
+    import paper_2506_02572_b200 as H
+    sh = case["shape"]
+    q = case["q"].to(device)
+    K = case["K"].to(device).contiguous()
+    V = case["V"].to(device).contiguous()
+    W = case["W"].to(device).contiguous()
+    kn, vn = case["k_new"].to(device), case["v_new"].to(device)
+    nb = (case["n_before"] if n_override is None else n_override).to(device)
+    B, Hkv, cap, d = K.shape
+    Wd = sh.rbits // 32
+    codes = torch.zeros(B, Hkv, cap, Wd, dtype=torch.int32, device=device)
+    H.hash_keys(K, W, codes, 0, int(nb.max().item()))
+    H.append(kn, vn, W, K, V, codes, nb)
+    n = nb + 1
+    n_max = int(n.max().item())
+    out_idx = torch.full((B, Hkv, k), -7, dtype=torch.int32, device=device)
+    out_score = torch.zeros(B, Hkv, k, dtype=torch.int32, device=device)
+    qcodes = torch.zeros(B, sh.Hq, Wd, dtype=torch.int32, device=device)
+    out = H.decode_topk_attn(q, K, V, codes, W, n, k, n_max=n_max, out_dtype=out_dtype, out_idx=out_idx,
+                             out_score=out_score, out_qcodes=qcodes)
+    torch.cuda.synchronize()
+    return dict(K=K.cpu(), V=V.cpu(), codes=codes.cpu(), out=out.cpu(), idx=out_idx.cpu(),
+                score=out_score.cpu(), qc=qcodes.cpu(), n=n.cpu())
+
+
+def check_codes(gpu_codes: np.ndarray, K64: np.ndarray, W64: np.ndarray, rows=None):
+    """Protocol step 1: GPU codes equal O1 except bits with |projection| < 1e-4.
+    gpu_codes/K64 are [R, W] / [R, d] for one KV head.  Returns (mismatch, near_zero, bits)."""
+    if rows is not None:
+        gpu_codes, K64 = gpu_codes[rows], K64[rows]
+    ref, nz = O.hash_encode(K64, W64)
+    rbit = W64.shape[1]
+    diff = O.bit_unpack(ref, rbit) != O.bit_unpack(gpu_codes, rbit)
+    assert not np.any(diff & ~nz), f"{int((diff & ~nz).sum())} code bits differ outside the near-zero band"
+    return int(diff.sum()), int(nz.sum()), diff.size
+
+
+def check_decode(case: dict, g: dict, k: int, code_rows_sample: int | None = None, rng_seed: int = 0):
+    """Full parity protocol on one decode step.  Returns stats dict."""
+    sh = case["shape"]
+    W64 = to_np64(case["W"])
+    B, Hkv = sh.B, sh.Hkv
+    G = sh.G
+    n = g["n"].numpy()
+    codes = codes_u32(g["codes"])
+    # the oracle's own caches: generator inputs + oracle append (Alg. 3 lines 3-4)
+    Wd = sh.rbits // 32
+    K64, V64, _, _ = O.append(to_np64(case["K"]), to_np64(case["V"]),
+                              np.zeros(case["K"].shape[:3] + (Wd,), np.uint32),
+                              to_np64(case["k_new"]), to_np64(case["v_new"]), W64, n - 1)
+    for b in range(B):
+        nb = int(n[b])
+        assert np.array_equal(to_np64(g["K"])[b, :, :nb], K64[b, :, :nb]), "K cache differs after append"
+        assert np.array_equal(to_np64(g["V"])[b, :, :nb], V64[b, :, :nb]), "V cache differs after append"
+    rng = np.random.default_rng(rng_seed)
+    mism = nzc = bits = 0
+    for b in range(B):
+        for h in range(Hkv):
+            nb = int(n[b])
+            rows = None
+            if code_rows_sample and nb > code_rows_sample:
+                rows = np.sort(rng.choice(nb, size=code_rows_sample, replace=False))
+                rows[-1] = nb - 1  # always include the appended token
+            m, z, nbits = check_codes(codes[b, h, :nb], K64[b, h, :nb], W64[h], rows)
+            mism += m; nzc += z; bits += nbits
+    assert nzc < 1e-4 * bits, f"near-zero bits {nzc} of {bits}"
+    # q codes (protocol step 1 for Q_H)
+    q64 = to_np64(case["q"])
+    qref, qnz = O.query_codes(q64, W64)
+    qg = codes_u32(g["qc"])
+    qdiff = O.bit_unpack(qref.reshape(-1, sh.rbits // 32), sh.rbits) != O.bit_unpack(qg.reshape(-1, sh.rbits // 32), sh.rbits)
+    assert not np.any(qdiff & ~qnz.reshape(qdiff.shape)), "query code bits differ outside the near-zero band"
+    # step 2: GPU codes into O3-O5 -> D, S, idx bit-exact
+    res = O.decode(q64, K64, V64, codes, W64, n, k, qc=qg)
+    idx = g["idx"].numpy()
+    sc = g["score"].numpy()
+    for b in range(B):
+        kp = min(k, int(n[b]))
+        for h in range(Hkv):
+            assert np.array_equal(idx[b, h, :kp], res["idx"][b][h]), f"index set differs at b={b} g={h}"
+            assert np.all(idx[b, h, kp:] == -1)
+            assert np.array_equal(sc[b, h, :kp], res["S"][b][h]), f"scores differ at b={b} g={h}"
+    # step 3: same indices -> outputs within tolerance
+    err = float(np.max(np.abs(g["out"].double().numpy() - res["out"])))
+    tol = TOL[sh.dtype]
+    assert err <= tol, f"max abs err {err} > {tol}"
+    return dict(code_bit_mismatch=mism, near_zero_bits=nzc, bits=bits, max_abs_err=err)

@@ -1,0 +1,82 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle, following
+the north_star protocol (codes bit-exact outside the near-zero band; given the
+GPU's codes, D/S/index sets bit-exact; outputs within 2e-3 bf16 / 1e-5 fp32)."""
+import dataclasses
+
+import pytest
+import torch
+
+import synth
+from tests.hata_testutil import check_decode, gpu_step
+
+pytestmark = pytest.mark.gpu
+
+
+def _shape(name, **kw):
+    return dataclasses.replace(synth.CONFIGS[name], **kw)
+
+
+SMALL = [
+    ("cfg1", synth.CONFIGS["cfg1"], "planted"),
+    ("g4_r128_8k", _shape("cfg2", N=8192 + 37, k=256), "planted"),
+    ("g4_r128_ragged_tail", _shape("cfg2", N=5000, k=300, B=2), "planted"),
+    ("g5_r256_small", _shape("cfg5", B=2, N=6000, k=200), "planted"),
+    ("g1_r32", _shape("cfg1", dtype="bf16", rbits=32, N=3000, k=100), "planted"),
+    ("g2_r64", _shape("cfg2", Hq=16, Hkv=8, rbits=64, N=4096, k=128), "planted"),
+    ("g8_r128", _shape("cfg2", Hq=64, Hkv=8, N=4000, k=129), "planted"),
+    ("f32_g4", _shape("cfg2", dtype="f32", N=3000, k=100), "plain"),
+    ("tie_equal", _shape("cfg2", N=4096, k=500), "equal"),
+    ("tie_pool8", _shape("cfg2", N=9000, k=700), "pool8"),
+    ("tie_dup", _shape("cfg2", N=8192, k=333), "dup"),
+    ("k_eq_n_dense", _shape("cfg2", N=2048, k=2048), "planted"),
+    ("k_gt_n", _shape("cfg2", N=700, k=1024), "planted"),
+    ("n_eq_1", _shape("cfg2", N=1, k=16), "plain"),
+]
+
+
+@pytest.mark.parametrize("name,shape,variant", SMALL, ids=[s[0] for s in SMALL])
+def test_decode_parity_small(name, shape, variant):
+    case = synth.make_case(shape, seed=11, variant=variant)
+    g = gpu_step(case, shape.k)
+    st = check_decode(case, g, shape.k)
+    print(name, st)
+
+
+def test_decode_parity_ragged_batch():
+    shape = _shape("cfg2", B=3, N=6000, k=400)
+    case = synth.make_case(shape, seed=5, cap=6000)
+    nb = torch.tensor([5999, 4000, 17], dtype=torch.int64)
+    case["n_before"] = nb
+    # append rows at n_before: take the new k/v from those rows of the generator's K/V
+    g = gpu_step(case, shape.k, n_override=nb)
+    st = check_decode(case, g, shape.k)
+    print(st)
+
+
+@pytest.mark.parametrize("name", ["cfg2", "cfg4"])
+def test_decode_parity_full_size(name):
+    """BASELINE sizes, bench launch configuration; codes sampled per head."""
+    shape = synth.CONFIGS[name]
+    case = synth.make_case(shape, seed=1)
+    g = gpu_step(case, shape.k)
+    st = check_decode(case, g, shape.k, code_rows_sample=65536)
+    print(name, st)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("name", ["cfg3", "cfg5"])
+def test_decode_parity_full_size_batched(name):
+    shape = synth.CONFIGS[name]
+    case = synth.make_case(shape, seed=2)
+    g = gpu_step(case, shape.k)
+    st = check_decode(case, g, shape.k, code_rows_sample=4096)
+    print(name, st)
+
+
+def test_bf16_output_dtype():
+    shape = _shape("cfg2", N=3000, k=100)
+    case = synth.make_case(shape, seed=3)
+    g32 = gpu_step(case, shape.k)
+    g16 = gpu_step(case, shape.k, out_dtype=torch.bfloat16)
+    assert torch.equal(g32["idx"], g16["idx"])
+    assert (g16["out"].float() - g32["out"]).abs().max().item() <= 2 ** -8 * g32["out"].abs().max().item() + 1e-6
