@@ -123,7 +123,7 @@ class Step:
         H.hash_keys(self.K, self.W, self.codes, 0, sh.N - 1)
         self.out = torch.empty(B, sh.Hq, d, dtype=torch.float32, device=device)
         ws = H.decode_workspace_size(B, sh.Hq, Hkv, d, sh.rbits, sh.N, sh.k, self.K.dtype)
-        self.ws = torch.empty(max(ws, 1), dtype=torch.uint8, device=device)
+        self.ws = torch.zeros(max(ws, 1), dtype=torch.uint8, device=device)
 
     def append(self):
         self.H.append(self.kn, self.vn, self.W, self.K, self.V, self.codes, self.pos)
@@ -334,14 +334,14 @@ def main():
     us_dec = r["t_dec"] / args.steps * 1e6
     achieved = bytes_step / (us_dec * 1e-6) / 1e9
     H = r["sets"][0].H
-    C = H.decode_cluster_size(sh.B, sh.Hq, sh.Hkv, sh.d, sh.rbits, sh.N, sh.k, r["sets"][0].K.dtype)
+    C = H.decode_ranks(sh.B, sh.Hq, sh.Hkv, sh.d, sh.rbits, sh.N, sh.k, r["sets"][0].K.dtype)
     line = {
         "metric": METRIC, "value": sh.B * args.steps / r["t_step"], "unit": "tokens/s (one attention layer)",
         "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": us_step / 1e3,
         "us_per_step": us_step, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": sh.dtype, "data": "synthetic (synth.make_case, seeds 1000-1015)",
         "config": {"workload": f"{sh.name}: {sh.note}", "B": sh.B, "Hq": sh.Hq, "Hkv": sh.Hkv, "d": sh.d,
-                   "rbits": sh.rbits, "N": sh.N, "k": sh.k, "cluster": C,
+                   "rbits": sh.rbits, "N": sh.N, "k": sh.k, "ranks_per_head": C,
                    "l2": f"rotating {N_SETS} distinct cache sets ({N_SETS} x {bytes_step / 1e6:.1f} MB step bytes "
                          f"> 126 MB L2)", "parallelism": "single GPU"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,

@@ -118,9 +118,12 @@ hata_status hata_append(const void* k_new, const void* v_new, hata_dtype dt, con
  *              -1 padding beyond k'.
  *   out_score  optional [B, H_kv, k] int32: S = G*rbits - 2D of those tokens.
  *   out_qcodes optional [B, H_q, rbits/32] uint32: the query codes used.
- *   workspace  device scratch of >= hata_decode_workspace_size(...) bytes
- *              (may be NULL when that size is 0).
- * One kernel launch: one thread-block cluster per (b, KV head).
+ *   workspace  device scratch of >= hata_decode_workspace_size(...) bytes,
+ *              256-byte aligned, ZERO-FILLED before its first use (every
+ *              launch leaves its synchronisation words zeroed again); one
+ *              workspace per concurrently running call.  May be NULL when
+ *              the size is 0.
+ * One cooperative kernel launch of M x (B*H_kv) CTAs (hata_decode_ranks()).
  * Errors: INVALID_ARG (k < 1, H_q % H_kv, rbits % 32, n_max < 0, nulls),
  *         UNSUPPORTED, WORKSPACE, CUDA.  n[b] == 0 yields zero output and
  *         out_idx all -1.
@@ -136,8 +139,9 @@ hata_status hata_decode_topk_attn(const void* q, const void* K, const void* V, h
 size_t hata_decode_workspace_size(int B, int H_q, int H_kv, int d, int rbits, int64_t n_max, int k,
                                   hata_dtype dt);
 
-/* Cluster size (CTAs per (b, KV head)) the decode launch will use; for tests/bench. */
-int hata_decode_cluster_size(int B, int H_q, int H_kv, int d, int rbits, int64_t n_max, int k, hata_dtype dt);
+/* Number of CTAs ("ranks") per (b, KV head) the decode launch will use, M;
+ * the grid is M x (B*H_kv) CTAs.  Host-only; for tests/bench. */
+int hata_decode_ranks(int B, int H_q, int H_kv, int d, int rbits, int64_t n_max, int k, hata_dtype dt);
 
 /* ========================================================================
  * Sequence-sharded decode (one rank owns a contiguous token range of every

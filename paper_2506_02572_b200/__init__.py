@@ -18,7 +18,7 @@ import torch
 from . import _lib
 from ._lib import HataError, Strides  # noqa: F401
 
-__all__ = ["hash_keys", "append", "decode_topk_attn", "decode_workspace_size", "decode_cluster_size",
+__all__ = ["hash_keys", "append", "decode_topk_attn", "decode_workspace_size", "decode_ranks",
            "shard_candidates", "shard_select", "shard_partial_attn", "shard_combine", "HataError", "lib"]
 
 
@@ -86,8 +86,8 @@ def decode_workspace_size(B, Hq, Hkv, d, rbits, n_max, k, dtype=torch.bfloat16) 
     return int(lib().hata_decode_workspace_size(B, Hq, Hkv, d, rbits, n_max, k, _dt_of(dtype)))
 
 
-def decode_cluster_size(B, Hq, Hkv, d, rbits, n_max, k, dtype=torch.bfloat16) -> int:
-    return int(lib().hata_decode_cluster_size(B, Hq, Hkv, d, rbits, n_max, k, _dt_of(dtype)))
+def decode_ranks(B, Hq, Hkv, d, rbits, n_max, k, dtype=torch.bfloat16) -> int:
+    return int(lib().hata_decode_ranks(B, Hq, Hkv, d, rbits, n_max, k, _dt_of(dtype)))
 
 
 def decode_topk_attn(q, K, V, codes, W, n, k: int, n_max: int | None = None, scale: float = 0.0, out=None,
@@ -106,7 +106,7 @@ def decode_topk_attn(q, K, V, codes, W, n, k: int, n_max: int | None = None, sca
         raise HataError("K and V must share strides")
     ws = decode_workspace_size(B, Hq, Hkv, d, rbits, n_max, k, K.dtype)
     if ws and (workspace is None or workspace.numel() * workspace.element_size() < ws):
-        workspace = torch.empty(ws, dtype=torch.uint8, device=q.device)
+        workspace = torch.zeros(ws, dtype=torch.uint8, device=q.device)
     _lib.check(lib().hata_decode_topk_attn(
         _p(q.contiguous()), _p(K), _p(V), _strides4(K), _dt(K), _p(codes), _strides4(codes), _p(W), B, Hq, Hkv, d,
         rbits, _p(n), n_max, k, scale, _p(out), _dt(out), _p(out_idx), _p(out_score), _p(out_qcodes),
@@ -121,7 +121,7 @@ def shard_candidates(q, codes, W, n_local, n_local_max: int, token_offset: int, 
     Hkv, rbits = codes.shape[1], W.shape[2]
     ws = decode_workspace_size(B, Hq, Hkv, d, rbits, n_local_max, k, q.dtype)
     if ws and (workspace is None or workspace.numel() * workspace.element_size() < ws):
-        workspace = torch.empty(ws, dtype=torch.uint8, device=q.device)
+        workspace = torch.zeros(ws, dtype=torch.uint8, device=q.device)
     _lib.check(lib().hata_shard_candidates(
         _p(q.contiguous()), _dt(q), _p(codes), _strides4(codes), _p(W), B, Hq, Hkv, d, rbits, _p(n_local),
         n_local_max, token_offset, k, _p(cand_D), _p(cand_idx), _p(workspace) if ws else None, ws,

@@ -138,10 +138,10 @@ size_t hata_decode_workspace_size(int B, int H_q, int H_kv, int d, int rbits, in
   return get_plan(B, H_q, H_kv, d, rbits, n_max, k, elem_bytes(dt)).ws_total;
 }
 
-int hata_decode_cluster_size(int B, int H_q, int H_kv, int d, int rbits, int64_t n_max, int k, hata_dtype dt) {
+int hata_decode_ranks(int B, int H_q, int H_kv, int d, int rbits, int64_t n_max, int k, hata_dtype dt) {
   if (B < 1 || H_kv < 1 || H_q < H_kv || H_q % H_kv || rbits % 32 || n_max < 0 || k < 1 || !dtype_ok(dt)) return 0;
   if (!shape_supported(d, rbits, H_q / H_kv)) return 0;
-  return get_plan(B, H_q, H_kv, d, rbits, n_max, k, elem_bytes(dt)).C;
+  return get_plan(B, H_q, H_kv, d, rbits, n_max, k, elem_bytes(dt)).M;
 }
 
 static hata_status decode_common(const void* q, const void* K, const void* V, hata_strides kvs, hata_dtype dt,
@@ -170,11 +170,8 @@ static hata_status decode_common(const void* q, const void* K, const void* V, ha
   p.scale = scale != 0.f ? scale : 1.0f / sqrtf((float)d);
   p.out = out; p.out_bf16 = out_dt == HATA_BF16;
   p.out_idx = out_idx; p.out_score = out_score; p.out_qcodes = out_qcodes;
-  uint8_t* ws = reinterpret_cast<uint8_t*>(workspace);
-  p.gD = pl.gD ? reinterpret_cast<uint16_t*>(ws) : nullptr;
-  p.gsel = pl.gsel ? reinterpret_cast<int32_t*>(ws + pl.ws_D) : nullptr;
   p.cand_mode = cand_mode; p.token_offset = token_offset; p.cand_D = cand_D;
-  return cuda_status(hata::launch_decode(p, pl, dt == HATA_BF16, reinterpret_cast<cudaStream_t>(stream)));
+  return cuda_status(hata::launch_decode(p, pl, workspace, dt == HATA_BF16, reinterpret_cast<cudaStream_t>(stream)));
 }
 
 hata_status hata_decode_topk_attn(const void* q, const void* K, const void* V, hata_strides kvs, hata_dtype dt,
@@ -224,7 +221,7 @@ hata_status hata_shard_partial_attn(const void* q, const void* K, const void* V,
   p.scale = scale != 0.f ? scale : 1.0f / sqrtf((float)d);
   p.partial = partial;
   const int G = H_q / H_kv;
-  const int GT = G <= 1 ? 1 : G <= 2 ? 2 : G <= 4 ? 4 : G <= 5 ? 5 : 8;
+  const int GT = hata::group_template(G);
   return cuda_status(hata::launch_partial_attn(p, GT, dt == HATA_BF16, reinterpret_cast<cudaStream_t>(stream)));
 }
 

@@ -1,18 +1,23 @@
 // Host-side planning + dispatch of the fused decode kernel (hata_decode.cuh).
 #include <cstdlib>
-#include <mutex>
 #include "hata_internal.h"
 #include "hata_decode.cuh"
 
 namespace hata {
 
+constexpr int SMEM_LIMIT = 227 * 1024;
+constexpr int ROWS_SMEM_MAX = 4096;            // selected rows per rank kept in smem
+
 int device_sm_count() {
   int dev = 0, n = 148;
-  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  if (cudaGetDevice(&dev) == cudaSuccess) {
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) n = 148;
+  }
+  cudaGetLastError();
   return n;
 }
 
-static int group_template(int G) {
+int group_template(int G) {
   if (G <= 1) return 1;
   if (G <= 2) return 2;
   if (G <= 4) return 4;
@@ -48,89 +53,121 @@ static DecodeKernel get_kernel(int is_bf16, int W, int GT) {
   return is_bf16 ? pick_w<__nv_bfloat16>(W, GT) : pick_w<float>(W, GT);
 }
 
-static DecodeParams shape_params(int B, int Hq, int Hkv, int d, int rbits, int C, int chunk, int rows_cap, bool gD,
-                                 bool gsel) {
-  DecodeParams p = {};
-  p.B = B; p.Hq = Hq; p.Hkv = Hkv; p.G = Hq / Hkv; p.d = d; p.rbits = rbits;
-  p.C = C; p.chunk = chunk; p.rows_cap = rows_cap; p.nbins = p.G * rbits + 1;
-  p.gD = gD ? reinterpret_cast<uint16_t*>(16) : nullptr;     // non-null marker for layout only
-  p.gsel = gsel ? reinterpret_cast<int32_t*>(16) : nullptr;
-  return p;
-}
+static size_t up256(size_t x) { return (x + 255) / 256 * 256; }
 
-DecodePlan plan_decode(int B, int Hq, int Hkv, int d, int rbits, int64_t n_max, int k, int elem_bytes) {
+// Decomposition + shared-memory + workspace plan (pure function of the shape
+// and the device's SM count; cached by the ABI layer).
+DecodePlan plan_decode(int B, int Hq, int Hkv, int d, int rbits, int64_t n_max, int k, int eb) {
   DecodePlan pl = {};
   const int G = Hq / Hkv;
   pl.GT = group_template(G);
   pl.nbins = G * rbits + 1;
+  const int GT = pl.GT > 0 ? pl.GT : 1;
   const int units = B * Hkv;
-  int C = device_sm_count() / (units > 0 ? units : 1);
-  if (C > 16) C = 16;
-  if (C < 1) C = 1;
-  const int64_t by_len = (n_max + 1023) / 1024;
-  if (by_len < C) C = (int)(by_len < 1 ? 1 : by_len);
-  if (const char* e = std::getenv("HATA_CLUSTER")) {
-    int v = std::atoi(e);
-    if (v >= 1 && v <= 16) C = v;
+  const int sms = device_sm_count();
+  int M = sms / (units > 0 ? units : 1);
+  if (M < 1) M = 1;
+  if (M > DEC_MAX_RANKS) M = DEC_MAX_RANKS;
+  const int64_t by_len = (n_max + 1023) / 1024;          // >= 1024 tokens per rank
+  if (by_len < M) M = (int)(by_len < 1 ? 1 : by_len);
+  if (const char* e = std::getenv("HATA_RANKS")) {
+    const int v = std::atoi(e);
+    if (v >= 1 && v <= DEC_MAX_RANKS && v * units <= sms) M = v;
   }
-  const int W = rbits / 32;
-  DecodeKernel kern = get_kernel(elem_bytes == 2, W, pl.GT);
-  for (;;) {
-    int64_t per = (n_max + C - 1) / C;
-    pl.C = C;
-    pl.chunk = (int)((per + DEC_CHUNK_ALIGN - 1) / DEC_CHUNK_ALIGN * DEC_CHUNK_ALIGN);
-    if (pl.chunk < DEC_CHUNK_ALIGN) pl.chunk = DEC_CHUNK_ALIGN;
-    const int64_t kmax = k < n_max ? k : n_max;
-    pl.rows_cap = (int)((kmax + C - 1) / C);
-    if (pl.rows_cap < 1) pl.rows_cap = 1;
-    pl.gD = pl.chunk > DEC_D_SMEM_MAX;
-    pl.gsel = pl.rows_cap > DEC_SEL_SMEM_MAX;
-    DecodeParams sp = shape_params(B, Hq, Hkv, d, rbits, C, pl.chunk, pl.rows_cap, pl.gD, pl.gsel);
-    pl.smem = decode_smem_layout(sp, pl.GT > 0 ? pl.GT : 1, elem_bytes).total;
-    bool ok = true;
-    if (kern && C > 1) {
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, pl.smem);
-      cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-      cudaLaunchConfig_t cfg = {};
-      cudaLaunchAttribute at[1];
-      cfg.gridDim = dim3(C, units);
-      cfg.blockDim = dim3(DEC_THREADS);
-      cfg.dynamicSmemBytes = pl.smem;
-      at[0].id = cudaLaunchAttributeClusterDimension;
-      at[0].val.clusterDim.x = C; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
-      cfg.attrs = at; cfg.numAttrs = 1;
-      int ncl = 0;
-      // an error here means "no device to ask" (CPU-only build host): keep C
-      if (cudaOccupancyMaxActiveClusters(&ncl, (void*)kern, &cfg) == cudaSuccess && ncl < 1) ok = false;
-      cudaGetLastError();
-    }
-    if (ok || C == 1) break;
-    C = C > 8 ? 8 : C / 2;
+  const int region = DEC_RING_BYTES + ((d * rbits * eb + 127) & ~127);   // reusable after scoring
+  while (M > 1 && M * pl.nbins * 4 > region) --M;
+  pl.M = M;
+  const int64_t per = (n_max + M - 1) / M;
+  pl.chunk = (int)((per + DEC_CHUNK_ALIGN - 1) / DEC_CHUNK_ALIGN * DEC_CHUNK_ALIGN);
+  if (pl.chunk < DEC_CHUNK_ALIGN) pl.chunk = DEC_CHUNK_ALIGN;
+  const int64_t kmax = k < n_max ? k : n_max;
+  pl.R_cap = (int)((kmax + M - 1) / M);
+  if (pl.R_cap < 1) pl.R_cap = 1;
+  pl.rows_global = pl.R_cap > ROWS_SMEM_MAX;
+  const int rowb = d * eb + DEC_ROW_PAD;
+  int rc = region / (2 * rowb + GT * 4) - 1;
+  if (rc > pl.R_cap) rc = pl.R_cap;
+  if (rc < 1) rc = 1;
+  pl.rows_cap = rc;
+  // D in smem if the whole layout still fits
+  DecodeParams sp = {};
+  sp.d = d; sp.rbits = rbits; sp.nbins = pl.nbins; sp.chunk = pl.chunk; sp.rows_cap = pl.rows_cap;
+  sp.R_cap = pl.R_cap; sp.ws_rows = pl.rows_global ? reinterpret_cast<int32_t*>(256) : nullptr;
+  sp.d_smem = 1;
+  pl.smem = decode_smem_layout(sp, GT, eb).total;
+  pl.d_smem = pl.smem <= SMEM_LIMIT;
+  if (!pl.d_smem) {
+    sp.d_smem = 0;
+    pl.smem = decode_smem_layout(sp, GT, eb).total;
   }
-  pl.ws_D = pl.gD ? ((size_t)units * pl.C * pl.chunk * 2 + 255) / 256 * 256 : 0;
-  pl.ws_sel = pl.gsel ? ((size_t)units * pl.C * pl.rows_cap * 4 + 255) / 256 * 256 : 0;
-  pl.ws_total = pl.ws_D + pl.ws_sel;
+  // workspace (every section 256-byte aligned)
+  size_t off = 0;
+  pl.ws_sync = off;  off += M > 1 ? up256((size_t)units * 2 * 4) : 0;
+  pl.ws_hist = off;  off += M > 1 ? up256((size_t)units * M * pl.nbins * 4) : 0;
+  pl.ws_part = off;  off += M > 1 ? up256((size_t)units * M * GT * (d + 2) * 4) : 0;
+  pl.ws_D = off;     off += (M > 1 || !pl.d_smem) ? up256((size_t)units * M * pl.chunk * 2) : 0;
+  pl.ws_rows = off;  off += pl.rows_global ? up256((size_t)units * M * pl.R_cap * 4) : 0;
+  pl.ws_total = off;
   return pl;
 }
 
-cudaError_t launch_decode(DecodeParams& p, const DecodePlan& pl, int is_bf16, cudaStream_t s) {
+cudaError_t launch_decode(DecodeParams& p, const DecodePlan& pl, void* ws, int is_bf16, cudaStream_t s) {
   DecodeKernel kern = get_kernel(is_bf16, p.rbits / 32, pl.GT);
   if (!kern) return cudaErrorNotSupported;
-  p.C = pl.C; p.chunk = pl.chunk; p.rows_cap = pl.rows_cap; p.nbins = pl.nbins;
+  uint8_t* w = reinterpret_cast<uint8_t*>(ws);
+  p.M = pl.M; p.chunk = pl.chunk; p.nbins = pl.nbins; p.rows_cap = pl.rows_cap; p.R_cap = pl.R_cap;
+  p.d_smem = pl.d_smem;
+  p.ws_sync = pl.M > 1 ? reinterpret_cast<unsigned*>(w + pl.ws_sync) : nullptr;
+  p.ws_hist = pl.M > 1 ? reinterpret_cast<int32_t*>(w + pl.ws_hist) : nullptr;
+  p.ws_part = pl.M > 1 ? reinterpret_cast<float*>(w + pl.ws_part) : nullptr;
+  p.ws_D = (pl.M > 1 || !pl.d_smem) ? reinterpret_cast<uint16_t*>(w + pl.ws_D) : nullptr;
+  p.ws_rows = pl.rows_global ? reinterpret_cast<int32_t*>(w + pl.ws_rows) : nullptr;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, pl.smem);
   if (e != cudaSuccess) return e;
-  if (pl.C > 8) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   cudaLaunchConfig_t cfg = {};
-  cudaLaunchAttribute at[2];
-  cfg.gridDim = dim3(pl.C, p.B * p.Hkv);
+  cudaLaunchAttribute at[1];
+  cfg.gridDim = dim3(pl.M, p.B * p.Hkv);
   cfg.blockDim = dim3(DEC_THREADS);
   cfg.dynamicSmemBytes = pl.smem;
   cfg.stream = s;
-  at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = pl.C; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+  // ranks of a unit meet at a spin barrier: they must be co-resident
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = pl.M > 1 ? 1 : 0;
   cfg.attrs = at;
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, kern, (const DecodeParams)p);
+}
+
+// ---------------------------------------------------------------- shard phase 3
+typedef void (*PartialKernel)(const PartialParams);
+template <typename T>
+static PartialKernel pick_partial(int GT) {
+  switch (GT) {
+    case 1: return hata_partial_attn_kernel<T, 1, 128>;
+    case 2: return hata_partial_attn_kernel<T, 2, 128>;
+    case 4: return hata_partial_attn_kernel<T, 4, 128>;
+    case 5: return hata_partial_attn_kernel<T, 5, 128>;
+    case 8: return hata_partial_attn_kernel<T, 8, 128>;
+  }
+  return nullptr;
+}
+
+cudaError_t launch_partial_attn(PartialParams& p, int GT, int is_bf16, cudaStream_t s) {
+  PartialKernel kern = is_bf16 ? pick_partial<__nv_bfloat16>(GT) : pick_partial<float>(GT);
+  if (!kern) return cudaErrorNotSupported;
+  const int eb = is_bf16 ? 2 : 4;
+  const int rowb = p.d * eb + DEC_ROW_PAD;
+  const int QS = dec_qstride(p.d);
+  int rc = 192;
+  if (rc > p.k) rc = p.k;
+  p.rows_cap = rc;
+  const size_t smem = ((2 * (size_t)rc * rowb + 127) & ~(size_t)127) + (size_t)GT * rc * 4 + (size_t)GT * QS * 4 +
+                      32 * 4 + (size_t)p.k * 4;
+  if (smem > (size_t)SMEM_LIMIT) return cudaErrorNotSupported;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  kern<<<p.B * p.Hkv, DEC_THREADS, smem, s>>>(p);
+  return cudaGetLastError();
 }
 
 }  // namespace hata

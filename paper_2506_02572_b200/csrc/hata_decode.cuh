@@ -1,8 +1,16 @@
 // Fused HATA decode kernel: q-hash -> Hamming score + GQA aggregate -> exact
-// top-k (lowest index wins) -> gather + online-softmax attention -> split
-// combine, in ONE launch.  One thread-block cluster of C CTAs per (b, KV head);
-// every cross-CTA step goes through DSMEM + barrier.cluster (no global
-// atomics, no grid sync).
+// top-k (lowest index wins) -> gather + softmax attention -> split combine, in
+// ONE launch.
+//
+// Work decomposition: a "unit" is one (b, KV head);
+// each unit is served by M CTAs ("ranks") that own contiguous token chunks, so
+// the grid (M x units) covers the 148 SMs even when B*H_kv is small.  The
+// launch is cooperative (all CTAs co-resident) and the ranks of a unit meet
+// exactly once, at a global-memory barrier after scoring, to exchange their
+// D-histograms.  Every rank then derives the same threshold, per-rank tie
+// quotas and output offsets, takes an equal share of the k' selected rows
+// (re-scanning the D arrays it needs from L2), attends to them, and the last
+// rank to finish merges the M softmax partials in rank order.
 //
 // PAPER: Alg. 3 lines 6, 10-17; §4.
 // Readings R1-R20 are listed in DESIGN.md.
@@ -14,16 +22,18 @@ namespace hata {
 
 constexpr int DEC_THREADS = 256;
 constexpr int DEC_WARPS = DEC_THREADS / 32;
-constexpr int DEC_STAGE_BYTES = 16384;      // one bulk copy of codes
-constexpr int DEC_STAGES = 4;               // ring depth (64 KB)
+constexpr int DEC_STAGE_BYTES = 16384;       // one bulk copy of codes
+constexpr int DEC_STAGES = 6;                // code ring depth (96 KB in flight)
 constexpr int DEC_RING_BYTES = DEC_STAGE_BYTES * DEC_STAGES;
-constexpr int DEC_D_SMEM_MAX = 16384;       // tokens/CTA whose D (u16) lives in smem
-constexpr int DEC_SEL_SMEM_MAX = 4096;      // selected rows/CTA held in smem
-constexpr int DEC_CHUNK_ALIGN = 64;         // tokens
+constexpr int DEC_D_SMEM_MAX = 16384;        // tokens/CTA whose D (u16) stays in smem
+constexpr int DEC_CHUNK_ALIGN = 64;          // tokens
+constexpr int DEC_MAX_RANKS = 32;            // M cap (histogram exchange is M x nbins per rank)
+constexpr int DEC_ROW_PAD = 16;              // bytes of padding per staged K/V row (bank spread)
+constexpr int DEC_QS_PAD = 4;                // floats of padding per q row in smem
 
 struct DecodeParams {
   const void* q;           // [B, Hq, d] contiguous
-  const void* K;           // cache, element strides below, d contiguous
+  const void* K;           // caches, element strides, d contiguous
   const void* V;
   int64_t kv_sb, kv_sh, kv_st;
   const uint32_t* codes;   // [B, Hkv, cap, W] word strides, row stride == W
@@ -37,12 +47,19 @@ struct DecodeParams {
   int32_t* out_idx;        // [B, Hkv, k] or null
   int32_t* out_score;      // [B, Hkv, k] or null
   uint32_t* out_qcodes;    // [B, Hq, W] or null
-  uint16_t* gD;            // global D workspace [B*Hkv*C*chunk] or null (smem)
-  int32_t* gsel;           // global selected-list workspace [B*Hkv*C*rows_cap] or null (smem)
-  int C;                   // cluster size (CTAs per (b, g))
-  int chunk;               // tokens per CTA (capacity), multiple of DEC_CHUNK_ALIGN
+  // decomposition
+  int M;                   // ranks (CTAs) per unit
+  int chunk;               // tokens per rank (capacity), multiple of DEC_CHUNK_ALIGN
   int nbins;               // G*rbits + 1
-  int rows_cap;            // selected rows per CTA (capacity)
+  int rows_cap;            // rows per attention batch held in smem
+  int R_cap;               // selected rows per rank (capacity of the rows list)
+  int32_t* ws_rows;        // [units, M, R_cap] rows list when it does not fit in smem, else null
+  int d_smem;              // 1: this rank's D lives in smem (mirrored to ws_D when M > 1)
+  // workspace (global); zero-initialised once, left zeroed by every launch
+  int32_t* ws_hist;        // [units, M, nbins]            (M > 1)
+  uint16_t* ws_D;          // [units, M, chunk]            (M > 1 or !d_smem)
+  float* ws_part;          // [units, M, GT, d+2]          (M > 1)
+  unsigned* ws_sync;       // [units, 2]: barrier, done    (M > 1)
   // sequence-shard phase 1 (hata_shard_candidates): stop after the select and
   // emit (D, global index) candidates instead of attending.
   int cand_mode;
@@ -51,220 +68,285 @@ struct DecodeParams {
 };
 
 struct DecodeSmem {
-  int ring, bars, hist, D, qf, qw, planes, sel, red, pub, part, misc, total;
+  int ring, W, bars, hist, D, qf, qw, planes, rows, red, misc, total;
+  int hm, kv, sc, rb;      // aliases inside ring+W after scoring
 };
 
+__host__ __device__ inline int dec_qstride(int d) { return d + DEC_QS_PAD; }
+
 // Shared-memory carve-up; identical on host and device.
-__host__ __device__ inline DecodeSmem decode_smem_layout(const DecodeParams& p, int GT, int elem_bytes) {
+__host__ __device__ inline DecodeSmem decode_smem_layout(const DecodeParams& p, int GT, int eb) {
   auto up = [](int x) { return (x + 127) & ~127; };
   DecodeSmem s;
   int off = 0;
-  int wp = DEC_WARPS * GT * (p.d + 2) * 4;        // per-warp softmax partials (aliases ring)
-  int ring = DEC_RING_BYTES > wp ? DEC_RING_BYTES : wp;
-  (void)elem_bytes;
-  s.ring = off; off += up(ring);
-  s.bars = off; off += up(DEC_STAGES * 8 + 8);
+  s.ring = off; off += DEC_RING_BYTES;
+  s.W = off; off += up(p.d * p.rbits * eb);
+  s.bars = off; off += up((DEC_STAGES + 2) * 8);
   s.hist = off; off += up(p.nbins * 4);
-  s.D = off; off += (p.gD ? 0 : up(p.chunk * 2));
-  s.qf = off; off += up(GT * p.d * 4);
+  s.D = off; off += p.d_smem ? up(p.chunk * 2) : 0;
+  s.qf = off; off += up(GT * dec_qstride(p.d) * 4);
   s.qw = off; off += up(GT * (p.rbits / 32) * 4);
   s.planes = off; off += up(2 * 4 * 8 * 4);
-  s.sel = off; off += (p.gsel ? 0 : up(p.rows_cap * 4));
-  int sl = (p.nbins + p.C - 1) / p.C;
-  s.red = off; off += up((sl + 1) * 4);
-  s.pub = off; off += up(64 * 4);
-  s.part = off; off += up(GT * (p.d + 2) * 4);
+  s.rows = off; off += p.ws_rows ? 0 : up(p.R_cap * 4);
+  s.red = off; off += up((DEC_MAX_RANKS * 4 + 64) * 4);
   s.misc = off; off += up(64 * 4);
   s.total = off;
+  // after scoring the ring + W region is free:
+  //   hm  : [M][nbins] int32 histograms of all ranks (select phase)
+  //   kv  : staged K rows then V rows, [rows_cap][d*eb + pad] each (attention phase)
+  //   sc  : [GT][rows_cap] fp32 logits / probabilities
+  const int rowb = p.d * eb + DEC_ROW_PAD;
+  s.hm = 0;
+  s.kv = 0;
+  s.sc = up(2 * p.rows_cap * rowb);
+  s.rb = rowb;
   return s;
 }
 
-// Projection of one fp32 vector x[d] (smem) onto 32 consecutive hash bits
-// [bit0, bit0+32) of W_g, returned as one packed word (lane i -> bit i).
-// Alg. 2 (P:216-218): Sign(MatMul) then BitPack, LSB-first; sign(0) -> 1.
-template <typename T>
-__device__ __forceinline__ uint32_t hash_word_warp(const float* __restrict__ x, const T* __restrict__ Wg, int d,
-                                                   int rbits, int bit0, int lane) {
-  float acc = 0.f;
-  const T* col = Wg + bit0 + lane;
-#pragma unroll 8
-  for (int j = 0; j < d; ++j) acc = fmaf(x[j], Elem<T>::to_f(col[(int64_t)j * rbits]), acc);
-  return __ballot_sync(0xffffffffu, acc >= 0.f);
+// ----------------------------------------------------------------- helpers
+__device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem_dst)), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+// Order-preserving scan of one rank's D array (token order).  Tokens with
+// D < thr are selected; ties (D == thr) are selected while their tie rank is
+// below `quota`.  Each selected token gets position pos = base + #selected
+// before it in this chunk; positions in [P0, P1) are emitted via `emit`.
+// All threads of the block must call (block-uniform arguments).
+template <typename Emit>
+__device__ __forceinline__ void scan_chunk(const uint16_t* Dc, bool from_global, int L, int thr, int quota, int base,
+                                           int P0, int P1, int* wcnt, Emit emit) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int seg = ((L + DEC_WARPS - 1) / DEC_WARPS + 31) & ~31;
+  const int s0 = min(L, warp * seg), s1 = min(L, s0 + seg);
+  auto ldD = [&](int j) -> int {
+    if (j >= s1) return 0x7fffffff;
+    return from_global ? (int)__ldcg(Dc + j) : (int)Dc[j];
+  };
+  int lt_w = 0, ti_w = 0;
+  for (int j0 = s0; j0 < s1; j0 += 32) {
+    const int Dv = ldD(j0 + lane);
+    lt_w += __popc(__ballot_sync(0xffffffffu, Dv < thr));
+    ti_w += __popc(__ballot_sync(0xffffffffu, Dv == thr));
+  }
+  __syncthreads();                      // wcnt reuse guard
+  if (lane == 0) { wcnt[2 * warp] = lt_w; wcnt[2 * warp + 1] = ti_w; }
+  __syncthreads();
+  int lt_b = 0, ti_b = 0;
+  for (int w = 0; w < warp; ++w) { lt_b += wcnt[2 * w]; ti_b += wcnt[2 * w + 1]; }
+  // skip whole segments whose positions fall outside [P0, P1) (warp-uniform)
+  const int seg_first = base + lt_b + min(ti_b, quota);
+  const int seg_last = base + lt_b + lt_w + min(ti_b + ti_w, quota);  // exclusive
+  if (seg_last <= P0 || seg_first >= P1) return;
+  for (int j0 = s0; j0 < s1; j0 += 32) {
+    const int j = j0 + lane;
+    const int Dv = ldD(j);
+    const uint32_t lm = __ballot_sync(0xffffffffu, Dv < thr);
+    const uint32_t tm = __ballot_sync(0xffffffffu, Dv == thr);
+    const uint32_t below_me = (1u << lane) - 1u;
+    const int tr = ti_b + __popc(tm & below_me);
+    if (Dv < thr || (Dv == thr && tr < quota)) {
+      const int pos = base + lt_b + __popc(lm & below_me) + min(tr, quota);
+      if (pos >= P0 && pos < P1) emit(pos, j, Dv);
+    }
+    lt_b += __popc(lm);
+    ti_b += __popc(tm);
+  }
 }
 
-// Gather + online softmax over `Rr` selected rows (indices in `rows`), all G
-// heads of the group; result = this CTA's partial (m, l, acc[d]) per head in
-// `part` ([GT][d+2]).  Alg. 3 lines 14-17 with the gather fused
-// into the attention loop: rows are never materialised in HBM.
-// `wp` is >= DEC_WARPS*GT*(d+2) floats of scratch.  All threads must call.
+// Per-thread slice of the attention output: head h, elements 2*e2, 2*e2+1.
+template <int GT, int D_HEAD>
+struct AttnState {
+  static constexpr int NSL = (GT * D_HEAD / 2 + DEC_THREADS - 1) / DEC_THREADS;  // slices per thread
+  float acc[NSL][2];
+};
+
+// Softmax attention of the G heads over `Rr` rows whose cache indices are in
+// rows[0..Rr) (smem), in batches of `rows_cap` rows staged in smem with
+// cp.async -- the gather is fused into the attention: selected rows
+// never land in HBM.  Logits: fp32 FMA over exact bf16 products; softmax and
+// P.V in fp32 (R14).  On return: m_s[h], l_s[h] (smem, max logit and sum of
+// exp) and st.acc (registers, this thread's unnormalised output slices).
 template <typename T, int GT, int D_HEAD>
 __device__ __forceinline__ void attend_rows(const int32_t* rows, int Rr, const T* __restrict__ Kb,
                                             const T* __restrict__ Vb, int64_t kv_st, const float* qf, int G,
-                                            float scale, float* wp, float* part) {
-  constexpr int EPL = D_HEAD / 32;
+                                            float scale, uint8_t* kvbuf, float* sc, int rows_cap, int rowb,
+                                            float* m_s, float* l_s, float* corr_s, AttnState<GT, D_HEAD>& st) {
+  constexpr int EB = sizeof(T);
+  constexpr int CH = D_HEAD * EB / 16;          // 16-byte chunks per row
+  constexpr int NSL = AttnState<GT, D_HEAD>::NSL;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  float qreg[GT][EPL];
+  const int QS = dec_qstride(D_HEAD);
+  uint8_t* Ks = kvbuf;
+  uint8_t* Vs = kvbuf + rows_cap * rowb;
 #pragma unroll
-  for (int h = 0; h < GT; ++h)
-#pragma unroll
-    for (int e = 0; e < EPL; ++e) qreg[h][e] = (h < G) ? qf[h * D_HEAD + lane * EPL + e] * scale : 0.f;
-  float m_[GT], l_[GT], acc[GT][EPL];
-#pragma unroll
-  for (int h = 0; h < GT; ++h) {
-    m_[h] = -INFINITY; l_[h] = 0.f;
-#pragma unroll
-    for (int e = 0; e < EPL; ++e) acc[h][e] = 0.f;
-  }
-  constexpr int U = 4;                                                // rows in flight per warp
-  for (int i0 = warp * U; i0 < Rr; i0 += DEC_WARPS * U) {
-    float kv[U][EPL], vv[U][EPL];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      if (i0 + u < Rr) {
-        const int64_t t = rows[i0 + u];
-        load_row_slice<T, EPL>(Kb + t * kv_st + lane * EPL, kv[u]);
-        load_row_slice<T, EPL>(Vb + t * kv_st + lane * EPL, vv[u]);
-      }
+  for (int s = 0; s < NSL; ++s) st.acc[s][0] = st.acc[s][1] = 0.f;
+  if (tid < GT) { m_s[tid] = -INFINITY; l_s[tid] = 0.f; }
+  for (int r0 = 0; r0 < Rr; r0 += rows_cap) {
+    const int nb = min(rows_cap, Rr - r0);
+    __syncthreads();                            // previous batch fully consumed
+    for (int c = tid; c < nb * CH * 2; c += DEC_THREADS) {
+      const int which = c / (nb * CH);          // 0: K, 1: V
+      const int rc = c - which * nb * CH;
+      const int i = rc / CH, ch = rc % CH;
+      const int64_t t = rows[r0 + i];
+      const T* src = (which ? Vb : Kb) + t * kv_st + ch * (16 / EB);
+      cp_async16((which ? Vs : Ks) + i * rowb + ch * 16, src);
     }
+    cp_async_wait_all();
+    __syncthreads();
+    // logits z[h][i] = scale * q_h . K_i
+    for (int pidx = tid; pidx < nb * GT; pidx += DEC_THREADS) {
+      const int i = pidx % nb, h = pidx / nb;
+      float z = 0.f;
+      if (h < G) {
+        const uint8_t* kr = Ks + i * rowb;
+        const float* qh = qf + h * QS;
+#pragma unroll 4
+        for (int c = 0; c < CH; ++c) {
+          float kv[16 / EB];
+          if constexpr (EB == 2) {
+            const uint4 raw = *reinterpret_cast<const uint4*>(kr + c * 16);
+            const __nv_bfloat162* hh = reinterpret_cast<const __nv_bfloat162*>(&raw);
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      if (i0 + u < Rr) {
-#pragma unroll
-        for (int h = 0; h < GT; ++h) {
-          if (h < G) {
-            float z = 0.f;
-#pragma unroll
-            for (int e = 0; e < EPL; ++e) z = fmaf(qreg[h][e], kv[u][e], z);
-            z = warp_sum(z);
-            const float mn = fmaxf(m_[h], z);
-            const float a = expf(m_[h] - mn), pz = expf(z - mn);
-            l_[h] = l_[h] * a + pz;
-#pragma unroll
-            for (int e = 0; e < EPL; ++e) acc[h][e] = fmaf(acc[h][e], a, pz * vv[u][e]);
-            m_[h] = mn;
+            for (int e = 0; e < 4; ++e) { float2 f = __bfloat1622float2(hh[e]); kv[2 * e] = f.x; kv[2 * e + 1] = f.y; }
+          } else {
+            const float4 raw = *reinterpret_cast<const float4*>(kr + c * 16);
+            kv[0] = raw.x; kv[1] = raw.y; kv[2] = raw.z; kv[3] = raw.w;
           }
+#pragma unroll
+          for (int e = 0; e < 16 / EB; ++e) z = fmaf(qh[c * (16 / EB) + e], kv[e], z);
         }
+        z *= scale;
+      }
+      sc[h * rows_cap + i] = z;
+    }
+    __syncthreads();
+    // running max / rescale per head (warp h)
+    for (int h = warp; h < G; h += DEC_WARPS) {
+      float mb = -INFINITY;
+      for (int i = lane; i < nb; i += 32) mb = fmaxf(mb, sc[h * rows_cap + i]);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) mb = fmaxf(mb, __shfl_xor_sync(0xffffffffu, mb, o));
+      const float mo = m_s[h];
+      const float mn = fmaxf(mo, mb);
+      float ls = 0.f;
+      for (int i = lane; i < nb; i += 32) {
+        const float pz = expf(sc[h * rows_cap + i] - mn);
+        sc[h * rows_cap + i] = pz;
+        ls += pz;
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) ls += __shfl_xor_sync(0xffffffffu, ls, o);
+      if (lane == 0) {
+        const float cr = (mo == -INFINITY) ? 0.f : expf(mo - mn);
+        corr_s[h] = cr;
+        l_s[h] = l_s[h] * cr + ls;
+        m_s[h] = mn;
       }
     }
-  }
-  // merge the warps' partials in fixed warp order -> CTA partial (m, l, acc)
-  const int stride_h = D_HEAD + 2;
+    __syncthreads();
+    // acc[h][e] = corr * acc + sum_i p[h][i] * V[i][e]
 #pragma unroll
-  for (int h = 0; h < GT; ++h) {
-    if (h < G) {
-      float* dst = wp + (warp * GT + h) * stride_h;
-      if (lane == 0) { dst[0] = m_[h]; dst[1] = l_[h]; }
-#pragma unroll
-      for (int e = 0; e < EPL; ++e) dst[2 + lane * EPL + e] = acc[h][e];
+    for (int s = 0; s < NSL; ++s) {
+      const int sl = tid + s * DEC_THREADS;
+      const int h = sl / (D_HEAD / 2), e2 = sl % (D_HEAD / 2);
+      if (h < G) {
+        const float cr = corr_s[h];
+        float a0 = st.acc[s][0] * cr, a1 = st.acc[s][1] * cr;
+        const float* ph = sc + h * rows_cap;
+#pragma unroll 4
+        for (int i = 0; i < nb; ++i) {
+          float v0, v1;
+          if constexpr (EB == 2) {
+            const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(Vs + i * rowb + e2 * 4));
+            v0 = f.x; v1 = f.y;
+          } else {
+            const float2 f = *reinterpret_cast<const float2*>(Vs + i * rowb + e2 * 8);
+            v0 = f.x; v1 = f.y;
+          }
+          const float pz = ph[i];
+          a0 = fmaf(pz, v0, a0);
+          a1 = fmaf(pz, v1, a1);
+        }
+        st.acc[s][0] = a0; st.acc[s][1] = a1;
+      }
     }
   }
   __syncthreads();
-  for (int o = tid; o < G * stride_h; o += DEC_THREADS) {
-    const int h = o / stride_h, e = o % stride_h;
-    float M = -INFINITY;
-    for (int w = 0; w < DEC_WARPS; ++w) M = fmaxf(M, wp[(w * GT + h) * stride_h]);
-    float v = 0.f;
-    if (e == 0) v = M;
-    else {
-      for (int w = 0; w < DEC_WARPS; ++w) {
-        const float mw = wp[(w * GT + h) * stride_h];
-        const float sc = (mw == -INFINITY) ? 0.f : expf(mw - M);
-        v = fmaf(wp[(w * GT + h) * stride_h + e], sc, v);
-      }
-    }
-    part[h * stride_h + e] = v;
-  }
 }
 
-// Flash-decoding merge of the C CTA partials of a cluster, in rank order:
-// M = max m_c, L = sum l_c e^{m_c - M}, o = sum acc_c e^{m_c - M} / L.
-// Writes normalised outputs to out[(row_base + h) * d + e] (fp32 or bf16), or,
-// if `raw` is non-null, the merged partial (M, L, A) to raw[(row_base+h)*(d+2)].
-// Caller brackets with cluster.sync().
-template <int D_HEAD>
-__device__ __forceinline__ void cluster_combine(cg::cluster_group& cluster, float* part, int C, int r, int G,
-                                                int64_t row_base, void* out, int out_bf16, float* raw) {
-  const int tid = threadIdx.x;
-  const int stride_h = D_HEAD + 2;
-  const int nout = G * stride_h;                                      // includes the (m, l) slots
-  const int per_cta = (nout + C - 1) / C;
-  const int o_lo = r * per_cta, o_hi = min(nout, o_lo + per_cta);
-  const int segl = tid & 15;                                          // lane-in-segment = source rank
-  for (int ob = o_lo; ob < o_hi; ob += DEC_THREADS / 16) {          // uniform trip count
-    const int o = ob + (tid >> 4);
-    const bool valid = o < o_hi;
-    const int h = valid ? o / stride_h : 0, e = valid ? o % stride_h : 0;
-    float mc = -INFINITY, lc = 0.f, vc = 0.f;
-    if (valid && segl < C) {
-      const float* rp = cluster.map_shared_rank(part, segl) + h * stride_h;
-      mc = rp[0]; lc = rp[1]; vc = rp[e];
-    }
-    float M = mc;
-#pragma unroll
-    for (int s = 8; s > 0; s >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, s, 16));
-    const float sc = (mc == -INFINITY) ? 0.f : expf(mc - M);
-    float Ls = lc * sc, Vs = (e >= 1) ? vc * sc : 0.f;
-#pragma unroll
-    for (int s = 1; s < 16; s <<= 1) {
-      Ls += __shfl_xor_sync(0xffffffffu, Ls, s, 16);
-      Vs += __shfl_xor_sync(0xffffffffu, Vs, s, 16);
-    }
-    if (valid && segl == 0) {
-      if (raw) {
-        raw[(row_base + h) * stride_h + e] = (e == 0) ? M : Vs;
-      } else if (e >= 2) {
-        const float ov = (Ls > 0.f) ? Vs / Ls : 0.f;
-        const int64_t oi = (row_base + h) * D_HEAD + (e - 2);
-        if (out_bf16) reinterpret_cast<__nv_bfloat16*>(out)[oi] = __float2bfloat16_rn(ov);
-        else reinterpret_cast<float*>(out)[oi] = ov;
-      }
-    }
+// Projection of one fp32 vector x[d] (smem) onto 32 consecutive hash bits
+// [bit0, bit0+32) of W_g (smem), one packed word (lane i -> bit i).
+// Alg. 2 (P:216-218): Sign(MatMul) then BitPack, LSB-first; sign(0) -> 1.
+template <typename T>
+__device__ __forceinline__ uint32_t hash_word_smem(const float* __restrict__ x, const T* __restrict__ Ws, int d,
+                                                   int rbits, int bit0, int lane) {
+  float a0 = 0.f, a1 = 0.f;
+  const T* col = Ws + bit0 + lane;
+#pragma unroll 8
+  for (int j = 0; j < d; j += 2) {
+    a0 = fmaf(x[j], Elem<T>::to_f(col[j * rbits]), a0);
+    a1 = fmaf(x[j + 1], Elem<T>::to_f(col[(j + 1) * rbits]), a1);
   }
+  return __ballot_sync(0xffffffffu, (a0 + a1) >= 0.f);
 }
 
 template <typename T, int W, int GT, int D_HEAD>
 __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __grid_constant__ DecodeParams p) {
   constexpr int J = planes_for_group(GT);
-  constexpr int EPL = D_HEAD / 32;               // head elements per lane
   constexpr int STAGE_TOK = DEC_STAGE_BYTES / (W * 4);
+  constexpr int EB = sizeof(T);
+  constexpr int NSL = AttnState<GT, D_HEAD>::NSL;
   extern __shared__ __align__(1024) uint8_t smem[];
 
-  cg::cluster_group cluster = cg::this_cluster();
-  const int C = p.C;
-  const int r = (int)cluster.block_rank();
-  const int bg = blockIdx.y;
-  const int b = bg / p.Hkv, g = bg % p.Hkv;
+  const int M = p.M;
+  const int r = blockIdx.x;
+  const int u = blockIdx.y;
+  const int b = u / p.Hkv, g = u % p.Hkv;
   const int G = p.G;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const DecodeSmem L = decode_smem_layout(p, GT, sizeof(T));
+  const DecodeSmem L = decode_smem_layout(p, GT, EB);
+  const int QS = dec_qstride(D_HEAD);
 
   uint8_t* ring = smem + L.ring;
+  T* Ws = reinterpret_cast<T*>(smem + L.W);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.bars);
   uint32_t* hist = reinterpret_cast<uint32_t*>(smem + L.hist);
-  uint16_t* Dbuf = p.gD ? p.gD + ((int64_t)bg * C + r) * p.chunk : reinterpret_cast<uint16_t*>(smem + L.D);
+  uint16_t* Dglob = p.ws_D ? p.ws_D + ((int64_t)u * M + r) * p.chunk : nullptr;
+  uint16_t* Dloc = p.d_smem ? reinterpret_cast<uint16_t*>(smem + L.D) : Dglob;
   float* qf = reinterpret_cast<float*>(smem + L.qf);
   uint32_t* qw = reinterpret_cast<uint32_t*>(smem + L.qw);
   uint32_t* planes = reinterpret_cast<uint32_t*>(smem + L.planes);   // [2][4][8]
-  int32_t* sel = p.gsel ? p.gsel + ((int64_t)bg * C + r) * p.rows_cap : reinterpret_cast<int32_t*>(smem + L.sel);
-  uint32_t* red = reinterpret_cast<uint32_t*>(smem + L.red);
-  int32_t* pub = reinterpret_cast<int32_t*>(smem + L.pub);
-  float* part = reinterpret_cast<float*>(smem + L.part);              // [GT][d+2]: m, l, acc[d]
+  int32_t* rows = p.ws_rows ? p.ws_rows + ((int64_t)u * M + r) * p.R_cap : reinterpret_cast<int32_t*>(smem + L.rows);
+  int32_t* red = reinterpret_cast<int32_t*>(smem + L.red);
   int32_t* misc = reinterpret_cast<int32_t*>(smem + L.misc);
+  float* fmisc = reinterpret_cast<float*>(misc);
 
   const int64_t n = p.n[b];
   const int kp = (int)(n < (int64_t)p.k ? n : (int64_t)p.k);      // k' = min(k, n)  (R10)
-  // this CTA's token chunk [t0, t1)
-  int64_t per = ((n + C - 1) / C + DEC_CHUNK_ALIGN - 1) / DEC_CHUNK_ALIGN * DEC_CHUNK_ALIGN;
+  // rank chunks [rr*per, (rr+1)*per) of this sequence
+  int per = (int)(((n + M - 1) / M + DEC_CHUNK_ALIGN - 1) / DEC_CHUNK_ALIGN * DEC_CHUNK_ALIGN);
   if (per > p.chunk) per = p.chunk;
+  if (per < DEC_CHUNK_ALIGN) per = DEC_CHUNK_ALIGN;
+  auto chunk_len = [&](int rr) -> int {
+    const int64_t a = (int64_t)rr * per, z = min((int64_t)n, a + per);
+    return z > a ? (int)(z - a) : 0;
+  };
   const int64_t t0 = (int64_t)r * per;
-  const int64_t t1 = (t0 + per < n) ? t0 + per : n;
-  const int Lr = t1 > t0 ? (int)(t1 - t0) : 0;
+  const int Lr = chunk_len(r);
   const int nstages = (Lr + STAGE_TOK - 1) / STAGE_TOK;
   const uint32_t* cbase = p.codes + (int64_t)b * p.c_sb + (int64_t)g * p.c_sh;
 
-  // ---- phase 0: kick off the code stream (q-independent) before anything else
+  // ---- phase 0: start the code stream and the W_g copy (both q-independent)
   if (tid == 0) {
-    for (int s = 0; s < DEC_STAGES; ++s) mbar_init(&bars[s], 1);
+    for (int s = 0; s < DEC_STAGES + 1; ++s) mbar_init(&bars[s], 1);
     fence_mbar_init();
   }
   __syncthreads();
@@ -272,42 +354,41 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
     const int slot = s % DEC_STAGES;
     const int ntok = min(STAGE_TOK, Lr - s * STAGE_TOK);
     const uint32_t bytes = (uint32_t)(ntok * W * 4) & ~15u;
-    if (bytes) {
-      mbar_arrive_expect_tx(&bars[slot], bytes);
-      bulk_g2s(ring + slot * DEC_STAGE_BYTES, cbase + (t0 + (int64_t)s * STAGE_TOK) * W, bytes, &bars[slot]);
-    } else {
-      mbar_arrive_expect_tx(&bars[slot], 0);
-    }
+    mbar_arrive_expect_tx(&bars[slot], bytes);
+    if (bytes) bulk_g2s(ring + slot * DEC_STAGE_BYTES, cbase + (t0 + (int64_t)s * STAGE_TOK) * W, bytes, &bars[slot]);
   };
   if (tid == 0) {
+    const uint32_t wbytes = (uint32_t)(p.d * p.rbits * EB);
+    mbar_arrive_expect_tx(&bars[DEC_STAGES], wbytes);
+    bulk_g2s(Ws, reinterpret_cast<const T*>(p.Wh) + (int64_t)g * p.d * p.rbits, wbytes, &bars[DEC_STAGES]);
     for (int s = 0; s < DEC_STAGES && s < nstages; ++s) issue_stage(s);
   }
   for (int i = tid; i < p.nbins; i += DEC_THREADS) hist[i] = 0;
 
-  // ---- phase 1: q -> fp32 smem, hash the G query heads (Alg. 3 line 6)
-  const T* qg = reinterpret_cast<const T*>(p.q) + ((int64_t)b * p.Hq + (int64_t)g * G) * p.d;
-  for (int i = tid; i < G * p.d; i += DEC_THREADS) qf[i] = Elem<T>::to_f(qg[i]);
+  // ---- phase 1: hash the G query heads of the group (Alg. 3 line 6)
+  const T* qg = reinterpret_cast<const T*>(p.q) + ((int64_t)b * p.Hq + (int64_t)g * G) * D_HEAD;
+  for (int i = tid; i < G * D_HEAD; i += DEC_THREADS) qf[(i / D_HEAD) * QS + i % D_HEAD] = Elem<T>::to_f(qg[i]);
   __syncthreads();
-  const T* Wg = reinterpret_cast<const T*>(p.Wh) + (int64_t)g * p.d * p.rbits;
+  mbar_wait(&bars[DEC_STAGES], 0);
   for (int wi = warp; wi < G * W; wi += DEC_WARPS) {
     const int h = wi / W, w = wi % W;
-    uint32_t word = hash_word_warp<T>(qf + h * p.d, Wg, p.d, p.rbits, w * 32, lane);
+    const uint32_t word = hash_word_smem<T>(qf + h * QS, Ws, D_HEAD, p.rbits, w * 32, lane);
     if (lane == 0) {
       qw[h * W + w] = word;
       if (p.out_qcodes && r == 0) p.out_qcodes[((int64_t)b * p.Hq + g * G + h) * W + w] = word;
     }
   }
   __syncthreads();
-  // bit planes of c_b = #{h: q_h bit b set} and of G - c_b
+  // bit planes of c_b = #{h: q_h bit b set} and of G - c_b (hata_score.cuh)
   if (warp < W) {
     int c = 0;
     for (int h = 0; h < G; ++h) c += (qw[h * W + warp] >> lane) & 1u;
     const int gc = G - c;
 #pragma unroll
     for (int j = 0; j < J; ++j) {
-      uint32_t a = __ballot_sync(0xffffffffu, (c >> j) & 1);
-      uint32_t bb = __ballot_sync(0xffffffffu, (gc >> j) & 1);
-      if (lane == 0) { planes[0 * 32 + j * 8 + warp] = a; planes[1 * 32 + j * 8 + warp] = bb; }
+      const uint32_t a = __ballot_sync(0xffffffffu, (c >> j) & 1);
+      const uint32_t bb = __ballot_sync(0xffffffffu, (gc >> j) & 1);
+      if (lane == 0) { planes[j * 8 + warp] = a; planes[32 + j * 8 + warp] = bb; }
     }
   }
   __syncthreads();
@@ -318,6 +399,7 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
     for (int w = 0; w < W; ++w) { A[j][w] = planes[j * 8 + w]; Bp[j][w] = planes[32 + j * 8 + w]; }
 
   // ---- phase 2: Hamming score + GQA sum (Alg. 3 lines 10-11) + histogram
+  const bool mirror = (M > 1) && p.d_smem;          // D also needed by the other ranks
   for (int s = 0; s < nstages; ++s) {
     const int slot = s % DEC_STAGES;
     mbar_wait(&bars[slot], (s / DEC_STAGES) & 1);
@@ -325,164 +407,156 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
     const int copied = (int)(((uint32_t)(ntok * W * 4) & ~15u) / (W * 4));
     const uint32_t* st = reinterpret_cast<const uint32_t*>(ring + slot * DEC_STAGE_BYTES);
     const int base = s * STAGE_TOK;
-#pragma unroll 2
-    for (int j = tid; j < ntok; j += DEC_THREADS) {
-      uint32_t kc[W];
-      if (j < copied) {
-        if constexpr (W == 4) {
-          uint4 v = reinterpret_cast<const uint4*>(st)[j];
-          kc[0] = v.x; kc[1] = v.y; kc[2] = v.z; kc[3] = v.w;
-        } else if constexpr (W == 8) {
-          uint4 v0 = reinterpret_cast<const uint4*>(st)[2 * j], v1 = reinterpret_cast<const uint4*>(st)[2 * j + 1];
-          kc[0] = v0.x; kc[1] = v0.y; kc[2] = v0.z; kc[3] = v0.w; kc[4] = v1.x; kc[5] = v1.y; kc[6] = v1.z; kc[7] = v1.w;
-        } else {
+    // two tokens per thread per iteration -> one 32-bit store of a u16 pair
+    for (int j2 = tid; 2 * j2 < ntok; j2 += DEC_THREADS) {
+      uint32_t Dpair[2];
 #pragma unroll
-          for (int w = 0; w < W; ++w) kc[w] = st[j * W + w];
+      for (int x = 0; x < 2; ++x) {
+        const int j = 2 * j2 + x;
+        uint32_t kc[W];
+#pragma unroll
+        for (int w = 0; w < W; ++w) kc[w] = 0;
+        if (j < copied) {
+          if constexpr (W == 4) {
+            const uint4 v = reinterpret_cast<const uint4*>(st)[j];
+            kc[0] = v.x; kc[1] = v.y; kc[2] = v.z; kc[3] = v.w;
+          } else if constexpr (W == 8) {
+            const uint4 v0 = reinterpret_cast<const uint4*>(st)[2 * j], v1 = reinterpret_cast<const uint4*>(st)[2 * j + 1];
+            kc[0] = v0.x; kc[1] = v0.y; kc[2] = v0.z; kc[3] = v0.w; kc[4] = v1.x; kc[5] = v1.y; kc[6] = v1.z; kc[7] = v1.w;
+          } else {
+#pragma unroll
+            for (int w = 0; w < W; ++w) kc[w] = st[j * W + w];
+          }
+        } else if (j < ntok) {
+          const uint32_t* gp = cbase + (t0 + base + j) * W;
+#pragma unroll
+          for (int w = 0; w < W; ++w) kc[w] = __ldg(gp + w);
         }
-      } else {
-        const uint32_t* gp = cbase + (t0 + base + j) * W;
-#pragma unroll
-        for (int w = 0; w < W; ++w) kc[w] = __ldg(gp + w);
+        if (j < ntok) {
+          Dpair[x] = group_distance<W, J>(kc, A, Bp);
+          atomicAdd(&hist[Dpair[x]], 1u);
+        } else {
+          Dpair[x] = 0xffffu;
+        }
       }
-      const uint32_t D = group_distance<W, J>(kc, A, Bp);
-      Dbuf[base + j] = (uint16_t)D;
-      atomicAdd(&hist[D], 1u);
+      const uint32_t packed = Dpair[0] | (Dpair[1] << 16);
+      reinterpret_cast<uint32_t*>(Dloc + base)[j2] = packed;
+      if (mirror) reinterpret_cast<uint32_t*>(Dglob + base)[j2] = packed;
     }
     __syncthreads();
     if (tid == 0 && s + DEC_STAGES < nstages) issue_stage(s + DEC_STAGES);
   }
+  __syncthreads();
 
-  // ---- phase 3: exact top-k' by counting select over the cluster (Alg. 3 lines 12-13)
-  // threshold thr = D of the k'-th best token; all D < thr selected; ties at thr
-  // selected lowest index first (R8) via per-CTA quotas in rank (= index) order.
-  cluster.sync();                                                     // #1 histograms complete
-  const int SL = (p.nbins + C - 1) / C;
-  const int lo = r * SL, hi = min(p.nbins, lo + SL);
-  const int nsl = hi > lo ? hi - lo : 0;
-  for (int i = tid; i < SL + 1; i += DEC_THREADS) red[i] = 0;
-  __syncthreads();
-  for (int t = tid; t < nsl * C; t += DEC_THREADS) {
-    const int i = t % nsl, c = t / nsl;
-    const uint32_t* rh = cluster.map_shared_rank(hist, c);
-    atomicAdd(&red[i], rh[lo + i]);
-  }
-  __syncthreads();
-  if (warp == 0) {
-    uint32_t sum = 0;
-    for (int i = lane; i < nsl; i += 32) sum += red[i];
-    sum = (uint32_t)warp_sum_i((int)sum);
-    if (lane == 0) red[SL] = sum;                                     // slice total
-  }
-  cluster.sync();                                                     // #2 slice sums published
-  if (warp == 0) {
-    // locate the slice holding the k'-th smallest D
-    uint32_t tot = 0;
-    if (lane < C) tot = *cluster.map_shared_rank(red + SL, lane);
-    uint32_t incl = tot;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += v;
+  // ---- phase 3: exact top-k' (Alg. 3 lines 12-13) by counting select.
+  // threshold thr = D of the k'-th best token; all D < thr are selected; ties
+  // at thr are selected lowest index first (R8) via per-rank quotas in rank
+  // (= token) order.  The ranks of a unit exchange histograms once.
+  int32_t* hm = reinterpret_cast<int32_t*>(smem + L.hm);           // [M][nbins]  (ring+W area)
+  unsigned* sync = (M > 1) ? p.ws_sync + 2 * u : nullptr;
+  if (M > 1) {
+    int32_t* gh = p.ws_hist + ((int64_t)u * M + r) * p.nbins;
+    for (int i = tid; i < p.nbins; i += DEC_THREADS) gh[i] = (int32_t)hist[i];
+    __syncthreads();
+    if (tid == 0) {
+      __threadfence();
+      atomicAdd(sync, 1u);
+      while (ld_acquire_gpu(sync) < (unsigned)M) {
+      }
     }
-    const uint32_t want = (uint32_t)kp;
-    const uint32_t m = __ballot_sync(0xffffffffu, lane < C && incl >= want);
-    int sstar = m ? __ffs(m) - 1 : 0;
-    uint32_t before = __shfl_sync(0xffffffffu, incl - tot, sstar);
-    // scan the slice's reduced bins
-    const uint32_t* rr = cluster.map_shared_rank(red, sstar);
-    const int slo = sstar * SL, snb = min(p.nbins, slo + SL) - slo;
-    int thr = -1;
-    uint32_t below = 0;
-    for (int i0 = 0; i0 < snb && thr < 0; i0 += 32) {
-      uint32_t v = (i0 + lane < snb) ? rr[i0 + lane] : 0u;
-      uint32_t inc = v;
+    __syncthreads();
+    const int32_t* all = p.ws_hist + (int64_t)u * M * p.nbins;
+    for (int i = tid; i < M * p.nbins; i += DEC_THREADS) hm[i] = __ldcg(all + i);
+  } else {
+    for (int i = tid; i < p.nbins; i += DEC_THREADS) hm[i] = (int32_t)hist[i];
+  }
+  __syncthreads();
+  // total histogram (reuse `hist`)
+  for (int i = tid; i < p.nbins; i += DEC_THREADS) {
+    int s = 0;
+    for (int rr = 0; rr < M; ++rr) s += hm[rr * p.nbins + i];
+    hist[i] = (uint32_t)s;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    int before = 0, thr = -1, below = 0;
+    for (int i0 = 0; i0 < p.nbins && thr < 0; i0 += 32) {
+      const int v = (i0 + lane < p.nbins) ? (int)hist[i0 + lane] : 0;
+      int inc = v;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
-        uint32_t u = __shfl_up_sync(0xffffffffu, inc, o);
-        if (lane >= o) inc += u;
+        const int w2 = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += w2;
       }
-      const uint32_t mm = __ballot_sync(0xffffffffu, before + inc >= want && (i0 + lane < snb));
+      const uint32_t mm = __ballot_sync(0xffffffffu, before + inc >= kp && (i0 + lane < p.nbins));
       if (mm) {
         const int l = __ffs(mm) - 1;
-        thr = slo + i0 + l;
+        thr = i0 + l;
         below = __shfl_sync(0xffffffffu, before + inc - v, l);
       } else {
         before += __shfl_sync(0xffffffffu, inc, 31);
       }
     }
-    if (kp == 0) { thr = -1; below = 0; }
-    if (lane == 0) { misc[0] = thr; misc[1] = (int)below; }
+    if (kp <= 0) { thr = -1; below = 0; }
+    if (lane == 0) { misc[0] = thr; misc[1] = kp - below; }
   }
   __syncthreads();
   const int thr = misc[0];
-  const int need = kp - misc[1];                                      // ties to take at thr
-  // local: # tokens with D < thr, # ties at thr
-  if (warp == 0) {
-    uint32_t lt = 0;
-    for (int i = lane; i < thr; i += 32) lt += hist[i];
-    lt = (uint32_t)warp_sum_i((int)lt);
-    if (lane == 0) { pub[0] = (int)lt; pub[1] = thr >= 0 ? (int)hist[thr] : 0; }
+  const int need = misc[1];
+  // per-rank (below, ties): warp w handles ranks w, w+8, ...
+  int32_t* rb_below = red;                       // [M]
+  int32_t* rb_ties = red + DEC_MAX_RANKS;        // [M]
+  int32_t* rb_off = red + 2 * DEC_MAX_RANKS;     // [M]
+  int32_t* rb_quota = red + 3 * DEC_MAX_RANKS;   // [M]
+  for (int rr = warp; rr < M; rr += DEC_WARPS) {
+    int s = 0;
+    for (int i = lane; i < thr; i += 32) s += hm[rr * p.nbins + i];
+    s = warp_sum_i(s);
+    if (lane == 0) { rb_below[rr] = s; rb_ties[rr] = thr >= 0 ? hm[rr * p.nbins + thr] : 0; }
   }
-  cluster.sync();                                                     // #3 (below_r, ties_r) published
+  __syncthreads();
   if (warp == 0) {
-    int bl = 0, ti = 0;
-    if (lane < C) { const int32_t* rp = cluster.map_shared_rank(pub, lane); bl = rp[0]; ti = rp[1]; }
+    const int bl = lane < M ? rb_below[lane] : 0, ti = lane < M ? rb_ties[lane] : 0;
     int incl = ti;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      int v = __shfl_up_sync(0xffffffffu, incl, o);
+      const int v = __shfl_up_sync(0xffffffffu, incl, o);
       if (lane >= o) incl += v;
     }
-    const int tp = incl - ti;                                          // ties in lower ranks
-    const int quota = max(0, min(need - tp, ti));
-    const int contrib = (lane < r) ? bl + quota : 0;
-    const int offset = warp_sum_i(contrib);
-    const int myquota = __shfl_sync(0xffffffffu, quota, r);
-    if (lane == 0) { misc[2] = offset; misc[3] = myquota; }
-  }
-  __syncthreads();
-  const int offset_r = misc[2], quota_r = misc[3];
-  const int R = (kp + C - 1) / C;                                     // rows per CTA for attention
-  // order-preserving compaction: each warp owns a contiguous segment
-  const int seg = ((Lr + DEC_WARPS - 1) / DEC_WARPS + 31) & ~31;
-  const int s0 = min(Lr, warp * seg), s1 = min(Lr, s0 + seg);
-  int lt_w = 0, ti_w = 0;
-  for (int j0 = s0; j0 < s1; j0 += 32) {
-    const int j = j0 + lane;
-    const int Dv = j < s1 ? (int)Dbuf[j] : 0x7fffffff;
-    lt_w += __popc(__ballot_sync(0xffffffffu, Dv < thr));
-    ti_w += __popc(__ballot_sync(0xffffffffu, Dv == thr));
-  }
-  int* wcnt = misc + 8;                                               // [DEC_WARPS][2]
-  if (lane == 0) { wcnt[2 * warp] = lt_w; wcnt[2 * warp + 1] = ti_w; }
-  __syncthreads();
-  int lt_b = 0, ti_b = 0;
-  for (int w = 0; w < warp; ++w) { lt_b += wcnt[2 * w]; ti_b += wcnt[2 * w + 1]; }
-  int32_t* oidx = p.out_idx ? p.out_idx + (int64_t)bg * p.k : nullptr;
-  int32_t* osc = p.out_score ? p.out_score + (int64_t)bg * p.k : nullptr;
-  int32_t* ocd = p.cand_D ? p.cand_D + (int64_t)bg * p.k : nullptr;
-  const int Gr = G * p.rbits;
-  for (int j0 = s0; j0 < s1; j0 += 32) {
-    const int j = j0 + lane;
-    const int Dv = j < s1 ? (int)Dbuf[j] : 0x7fffffff;
-    const uint32_t lm = __ballot_sync(0xffffffffu, Dv < thr);
-    const uint32_t tm = __ballot_sync(0xffffffffu, Dv == thr);
-    const uint32_t below_me = (1u << lane) - 1u;
-    const int my_tie_rank = ti_b + __popc(tm & below_me);
-    const bool is_sel = (Dv < thr) || (Dv == thr && my_tie_rank < quota_r);
-    if (is_sel) {
-      const int lt_before = lt_b + __popc(lm & below_me);
-      const int P = offset_r + lt_before + min(my_tie_rank, quota_r);
-      const int tok = (int)(t0 + j);
-      const int dest = P / R, slot = P - dest * R;
-      if (p.gsel) p.gsel[((int64_t)bg * C + dest) * p.rows_cap + slot] = tok;
-      else *cluster.map_shared_rank(sel + slot, dest) = tok;
-      if (oidx) oidx[P] = (int32_t)(tok + p.token_offset);
-      if (osc) osc[P] = Gr - 2 * Dv;                                   // S = G*rbits - 2D
-      if (ocd) ocd[P] = Dv;
+    const int quota = max(0, min(need - (incl - ti), ti));
+    const int sel = bl + quota;
+    int inc2 = sel;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, inc2, o);
+      if (lane >= o) inc2 += v;
     }
-    lt_b += __popc(lm);
-    ti_b += __popc(tm);
+    if (lane < M) { rb_quota[lane] = quota; rb_off[lane] = inc2 - sel; }
+  }
+  __syncthreads();
+
+  // this rank's equal share of the ascending selection: positions [P0, P1)
+  const int R = (kp + M - 1) / M;
+  const int P0 = min(kp, r * R), P1 = min(kp, P0 + R);
+  int32_t* oidx = p.out_idx ? p.out_idx + (int64_t)u * p.k : nullptr;
+  int32_t* osc = p.out_score ? p.out_score + (int64_t)u * p.k : nullptr;
+  int32_t* ocd = p.cand_D ? p.cand_D + (int64_t)u * p.k : nullptr;
+  const int Gr = G * p.rbits;
+  int* wcnt = misc + 16;                         // [DEC_WARPS][2]
+  for (int c = 0; c < M && P1 > P0; ++c) {
+    const int off = rb_off[c], cnt = rb_below[c] + rb_quota[c];
+    if (cnt == 0 || off + cnt <= P0 || off >= P1) continue;    // block-uniform
+    const bool own = (c == r);
+    const bool fromg = !(own && p.d_smem);
+    const uint16_t* Dc = fromg ? p.ws_D + ((int64_t)u * M + c) * p.chunk : Dloc;
+    const int64_t ctok = (int64_t)c * per;
+    scan_chunk(Dc, fromg, chunk_len(c), thr, rb_quota[c], off, P0, P1, wcnt, [&](int pos, int j, int Dv) {
+      const int tok = (int)(ctok + j);
+      rows[pos - P0] = tok;
+      if (oidx) oidx[pos] = (int32_t)(tok + p.token_offset);
+      if (osc) osc[pos] = Gr - 2 * Dv;                       // S = G*rbits - 2D
+      if (ocd) ocd[pos] = Dv;
+    });
   }
   if (r == 0) {
     for (int i = kp + tid; i < p.k; i += DEC_THREADS) {
@@ -491,29 +565,87 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
       if (ocd) ocd[i] = 0x7fffffff;
     }
   }
-  cluster.sync();                                                     // #4 selected lists complete
+  __syncthreads();
 
-  if (p.cand_mode) {                                                  // sequence-shard phase 1 stops here
-    cluster.sync();
+  // ---- phase 4: gather + softmax attention over this rank's rows (Alg. 3 lines 14-17)
+  float* m_s = fmisc + 32;
+  float* l_s = fmisc + 40;
+  float* corr_s = fmisc + 48;
+  AttnState<GT, D_HEAD> st;
+  if (!p.cand_mode) {
+    const T* Kb = reinterpret_cast<const T*>(p.K) + (int64_t)b * p.kv_sb + (int64_t)g * p.kv_sh;
+    const T* Vb = reinterpret_cast<const T*>(p.V) + (int64_t)b * p.kv_sb + (int64_t)g * p.kv_sh;
+    float* sc = reinterpret_cast<float*>(smem + L.sc);
+    attend_rows<T, GT, D_HEAD>(rows, P1 - P0, Kb, Vb, p.kv_st, qf, G, p.scale, smem + L.kv, sc, p.rows_cap, L.rb,
+                               m_s, l_s, corr_s, st);
+  }
+
+  // ---- phase 5: merge the M rank partials in rank order (flash-decoding combine)
+  const int64_t orow = (int64_t)b * p.Hq + (int64_t)g * G;      // first output row of the group
+  auto store_out = [&](int h, int e, float v) {
+    const int64_t oi = (orow + h) * D_HEAD + e;
+    if (p.out_bf16) reinterpret_cast<__nv_bfloat16*>(p.out)[oi] = __float2bfloat16_rn(v);
+    else reinterpret_cast<float*>(p.out)[oi] = v;
+  };
+  if (M == 1) {
+    if (!p.cand_mode) {
+#pragma unroll
+      for (int s = 0; s < NSL; ++s) {
+        const int sl = tid + s * DEC_THREADS;
+        const int h = sl / (D_HEAD / 2), e2 = sl % (D_HEAD / 2);
+        if (h < G) {
+          const float l = l_s[h];
+          store_out(h, 2 * e2, l > 0.f ? st.acc[s][0] / l : 0.f);
+          store_out(h, 2 * e2 + 1, l > 0.f ? st.acc[s][1] / l : 0.f);
+        }
+      }
+    }
     return;
   }
-  cluster.sync();                                                     // #4 selected lists complete
-
-  // ---- phase 4: gather + online-softmax attention over this CTA's rows (Alg. 3 lines 14-17)
-  const int row0 = r * R;
-  const int Rr = max(0, min(R, kp - row0));
-  const T* Kb = reinterpret_cast<const T*>(p.K) + (int64_t)b * p.kv_sb + (int64_t)g * p.kv_sh;
-  const T* Vb = reinterpret_cast<const T*>(p.V) + (int64_t)b * p.kv_sb + (int64_t)g * p.kv_sh;
-  __syncthreads();                                                    // ring becomes attention scratch
-  attend_rows<T, GT, D_HEAD>(sel, Rr, Kb, Vb, p.kv_st, qf, G, p.scale, reinterpret_cast<float*>(ring), part);
-  cluster.sync();                                                     // #5 CTA partials published
-  // ---- phase 5: combine the C partials in rank order (flash-decoding merge)
-  cluster_combine<D_HEAD>(cluster, part, C, r, G, ((int64_t)b * p.Hq + g * G), p.out, p.out_bf16, nullptr);
-  cluster.sync();                                                     // #6 keep smem alive for readers
+  const int PS = D_HEAD + 2;
+  float* mypart = p.ws_part + ((int64_t)u * M + r) * GT * PS;
+  if (!p.cand_mode) {
+#pragma unroll
+    for (int s = 0; s < NSL; ++s) {
+      const int sl = tid + s * DEC_THREADS;
+      const int h = sl / (D_HEAD / 2), e2 = sl % (D_HEAD / 2);
+      if (h < G) { mypart[h * PS + 2 + 2 * e2] = st.acc[s][0]; mypart[h * PS + 3 + 2 * e2] = st.acc[s][1]; }
+    }
+    if (tid < G) { mypart[tid * PS] = m_s[tid]; mypart[tid * PS + 1] = l_s[tid]; }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    const unsigned prev = atomicAdd(sync + 1, 1u);
+    misc[2] = (prev == (unsigned)(M - 1));
+  }
+  __syncthreads();
+  if (!misc[2]) return;
+  // last rank: all other partials are visible (their fence + the counter)
+  __threadfence();
+  if (!p.cand_mode) {
+    const float* parts = p.ws_part + (int64_t)u * M * GT * PS;
+    for (int o = tid; o < G * D_HEAD; o += DEC_THREADS) {
+      const int h = o / D_HEAD, e = o % D_HEAD;
+      float Mx = -INFINITY;
+      for (int rr = 0; rr < M; ++rr) Mx = fmaxf(Mx, __ldcg(parts + (rr * GT + h) * PS));
+      float Ls = 0.f, As = 0.f;
+      for (int rr = 0; rr < M; ++rr) {
+        const float* pr = parts + (rr * GT + h) * PS;
+        const float mr = __ldcg(pr);
+        const float scl = (mr == -INFINITY) ? 0.f : expf(mr - Mx);
+        Ls = fmaf(__ldcg(pr + 1), scl, Ls);
+        As = fmaf(__ldcg(pr + 2 + e), scl, As);
+      }
+      store_out(h, e, Ls > 0.f ? As / Ls : 0.f);
+    }
+  }
+  if (tid == 0) { sync[0] = 0u; sync[1] = 0u; }     // leave the workspace zeroed for the next launch
 }
 
 // ---------------------------------------------------------------------------
-// Sequence-shard phase 3: partial attention over this rank's selected rows.
+// Sequence-shard phase 3: attention over this rank's selected rows -> raw
+// (m, l, acc) partials.  One CTA per (b, KV head); rows in smem batches.
 struct PartialParams {
   const void* q;
   const void* K;
@@ -524,31 +656,52 @@ struct PartialParams {
   int B, Hq, Hkv, G, d, k;
   float scale;
   float* partial;          // [B, Hq, d+2]
-  int C;
+  int rows_cap;            // rows per smem batch
 };
 
 template <typename T, int GT, int D_HEAD>
 __global__ void __launch_bounds__(DEC_THREADS, 1) hata_partial_attn_kernel(const __grid_constant__ PartialParams p) {
-  extern __shared__ __align__(16) float psm[];
-  cg::cluster_group cluster = cg::this_cluster();
-  const int C = p.C, r = (int)cluster.block_rank();
-  const int bg = blockIdx.y, b = bg / p.Hkv, g = bg % p.Hkv, G = p.G;
-  float* qf = psm;                                  // [GT][d]
-  float* part = qf + GT * D_HEAD;                   // [GT][d+2]
-  float* wp = part + GT * (D_HEAD + 2);             // [DEC_WARPS][GT][d+2]
+  extern __shared__ __align__(1024) uint8_t psm[];
+  constexpr int EB = sizeof(T);
+  constexpr int NSL = AttnState<GT, D_HEAD>::NSL;
+  const int u = blockIdx.x, b = u / p.Hkv, g = u % p.Hkv, G = p.G;
+  const int tid = threadIdx.x;
+  const int QS = dec_qstride(D_HEAD);
+  const int rowb = D_HEAD * EB + DEC_ROW_PAD;
+  uint8_t* kv = psm;                                                         // [2][rows_cap][rowb]
+  float* sc = reinterpret_cast<float*>(psm + ((2 * p.rows_cap * rowb + 127) & ~127));   // [GT][rows_cap]
+  float* qf = sc + GT * p.rows_cap;                                          // [GT][QS]
+  float* fm = qf + GT * QS;                                                  // m, l, corr
+  int32_t* rows = reinterpret_cast<int32_t*>(fm + 32);                       // [k]
   const T* qg = reinterpret_cast<const T*>(p.q) + ((int64_t)b * p.Hq + (int64_t)g * G) * D_HEAD;
-  for (int i = threadIdx.x; i < G * D_HEAD; i += DEC_THREADS) qf[i] = Elem<T>::to_f(qg[i]);
-  const int cnt = p.own_cnt[bg];
-  const int R = (cnt + C - 1) / C;
-  const int Rr = max(0, min(R, cnt - r * R));
+  for (int i = tid; i < G * D_HEAD; i += DEC_THREADS) qf[(i / D_HEAD) * QS + i % D_HEAD] = Elem<T>::to_f(qg[i]);
+  const int cnt = p.own_cnt[u];
+  for (int i = tid; i < cnt; i += DEC_THREADS) rows[i] = p.own_idx[(int64_t)u * p.k + i];
   __syncthreads();
   const T* Kb = reinterpret_cast<const T*>(p.K) + (int64_t)b * p.kv_sb + (int64_t)g * p.kv_sh;
   const T* Vb = reinterpret_cast<const T*>(p.V) + (int64_t)b * p.kv_sb + (int64_t)g * p.kv_sh;
-  attend_rows<T, GT, D_HEAD>(p.own_idx + (int64_t)bg * p.k + (int64_t)r * R, Rr, Kb, Vb, p.kv_st, qf, G, p.scale,
-                             wp, part);
-  cluster.sync();
-  cluster_combine<D_HEAD>(cluster, part, C, r, G, (int64_t)b * p.Hq + g * G, nullptr, 0, p.partial);
-  cluster.sync();
+  AttnState<GT, D_HEAD> st;
+  float* m_s = fm;
+  float* l_s = fm + 8;
+  float* corr_s = fm + 16;
+  attend_rows<T, GT, D_HEAD>(rows, cnt, Kb, Vb, p.kv_st, qf, G, p.scale, kv, sc, p.rows_cap, rowb, m_s, l_s, corr_s,
+                             st);
+  const int PS = D_HEAD + 2;
+#pragma unroll
+  for (int s = 0; s < NSL; ++s) {
+    const int sl = tid + s * DEC_THREADS;
+    const int h = sl / (D_HEAD / 2), e2 = sl % (D_HEAD / 2);
+    if (h < G) {
+      float* pr = p.partial + ((int64_t)b * p.Hq + g * G + h) * PS;
+      pr[2 + 2 * e2] = st.acc[s][0];
+      pr[3 + 2 * e2] = st.acc[s][1];
+    }
+  }
+  if (tid < G) {
+    float* pr = p.partial + ((int64_t)b * p.Hq + g * G + tid) * PS;
+    pr[0] = m_s[tid];
+    pr[1] = l_s[tid];
+  }
 }
 
 }  // namespace hata

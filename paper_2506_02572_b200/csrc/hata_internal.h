@@ -36,14 +36,14 @@ cudaError_t launch_hash_keys_simt(const HashKeysParams& p, int is_bf16, cudaStre
 cudaError_t launch_hash_keys_tc(const HashKeysParams& p, cudaStream_t s);
 
 struct DecodePlan {
-  int C, chunk, rows_cap, nbins, GT;
-  bool gD, gsel;
-  size_t ws_D, ws_sel, ws_total;
-  int smem;
+  int M, chunk, R_cap, rows_cap, nbins, GT, smem;
+  bool d_smem, rows_global;
+  size_t ws_sync, ws_hist, ws_part, ws_D, ws_rows, ws_total;   // workspace byte offsets / size
 };
 struct DecodeParams;
 DecodePlan plan_decode(int B, int Hq, int Hkv, int d, int rbits, int64_t n_max, int k, int elem_bytes);
-cudaError_t launch_decode(DecodeParams& p, const DecodePlan& plan, int is_bf16, cudaStream_t s);
+int group_template(int G);
+cudaError_t launch_decode(DecodeParams& p, const DecodePlan& plan, void* ws, int is_bf16, cudaStream_t s);
 
 struct SelectParams {
   const int32_t* all_D;    // [P, B, Hkv, k]

@@ -6,7 +6,7 @@
 // PAPER: Alg. 3 lines 12-17 distributed over token ranges; the
 // paper itself is single-GPU, so the split is this build's.
 #include "hata_internal.h"
-#include "hata_decode.cuh"
+#include "hata_common.cuh"
 
 namespace hata {
 
@@ -154,45 +154,6 @@ cudaError_t launch_shard_combine(const float* part, int P, int B, int Hq, int d,
   else
     shard_combine_kernel<float><<<B * Hq, 128, 0, s>>>(part, P, B * Hq, d, reinterpret_cast<float*>(out));
   return cudaGetLastError();
-}
-
-typedef void (*PartialKernel)(const PartialParams);
-template <typename T>
-static PartialKernel pick_partial(int GT) {
-  switch (GT) {
-    case 1: return hata_partial_attn_kernel<T, 1, 128>;
-    case 2: return hata_partial_attn_kernel<T, 2, 128>;
-    case 4: return hata_partial_attn_kernel<T, 4, 128>;
-    case 5: return hata_partial_attn_kernel<T, 5, 128>;
-    case 8: return hata_partial_attn_kernel<T, 8, 128>;
-  }
-  return nullptr;
-}
-
-cudaError_t launch_partial_attn(PartialParams& p, int GT, int is_bf16, cudaStream_t s) {
-  PartialKernel kern = is_bf16 ? pick_partial<__nv_bfloat16>(GT) : pick_partial<float>(GT);
-  if (!kern) return cudaErrorNotSupported;
-  const int units = p.B * p.Hkv;
-  int C = device_sm_count() / (units > 0 ? units : 1);
-  if (C > 8) C = 8;
-  if (C < 1) C = 1;
-  const int64_t by_rows = (p.k + 127) / 128;
-  if (by_rows < C) C = (int)(by_rows < 1 ? 1 : by_rows);
-  p.C = C;
-  const int smem = (GT * 128 + GT * 130 + DEC_WARPS * GT * 130) * 4;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  if (e != cudaSuccess) return e;
-  cudaLaunchConfig_t cfg = {};
-  cudaLaunchAttribute at[1];
-  cfg.gridDim = dim3(C, units);
-  cfg.blockDim = dim3(DEC_THREADS);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = s;
-  at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = C; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, (const PartialParams)p);
 }
 
 }  // namespace hata
