@@ -134,6 +134,24 @@ hata_status hata_decode_topk_attn(const void* q, const void* K, const void* V, h
                                   hata_dtype out_dt, int32_t* out_idx, int32_t* out_score, uint32_t* out_qcodes,
                                   void* workspace, size_t ws_bytes, hata_stream_t stream);
 
+/* ------------------------------------------------------------------------
+ * hata_decode_step -- hata_append + hata_decode_topk_attn in ONE launch:
+ * the whole of Alg. 3 (lines 2-17) with the Encode & Cache update
+ * fused into the decode kernel (§4 "Kernel fusion for hash encoding").
+ *   k_new, v_new [B, H_kv, d] (dtype dt, 16-byte aligned): the new token's key
+ *                and value; written with HashEncode(k_new) at row n[b]-1 of
+ *                K, V and codes, then scored like every cached token (R11).
+ *   n            DEVICE int64 [B]: tokens per sequence INCLUDING the new one.
+ *   cap          rows allocated per (b, KV head); n_max > cap -> CAPACITY.
+ * Every other argument as for hata_decode_topk_attn; the result equals
+ * hata_append followed by hata_decode_topk_attn.
+ * ------------------------------------------------------------------------ */
+hata_status hata_decode_step(const void* q, const void* k_new, const void* v_new, void* K, void* V, hata_strides kvs,
+                             hata_dtype dt, uint32_t* codes, hata_strides cs, const void* W, int B, int H_q, int H_kv,
+                             int d, int rbits, const int64_t* n, int64_t n_max, int64_t cap, int k, float scale,
+                             void* out, hata_dtype out_dt, int32_t* out_idx, int32_t* out_score,
+                             uint32_t* out_qcodes, void* workspace, size_t ws_bytes, hata_stream_t stream);
+
 /* Bytes of device workspace hata_decode_topk_attn needs for this shape
  * (0 when everything fits on chip).  Host-only; never fails (0 on bad args). */
 size_t hata_decode_workspace_size(int B, int H_q, int H_kv, int d, int rbits, int64_t n_max, int k,
@@ -194,6 +212,13 @@ const char* hata_status_string(hata_status s);
 const char* hata_last_error(void);
 /* Library version string. */
 const char* hata_version(void);
+
+/* Diagnostics only.  buf: NULL (off, the default) or device memory of at least
+ * 16 * (number of decode CTAs) uint64; while set, every decode launch writes
+ * %globaltimer stamps (ns) of its phase boundaries to buf[cta * 16 + phase]
+ * (0 start, 1 q-hash done, 2 score done, 3 histograms exchanged, 4 D staged,
+ * 5 selection done, 6 attention done, 7 end).  Not for production use. */
+hata_status hata_debug_trace(void* buf);
 
 #ifdef __cplusplus
 }

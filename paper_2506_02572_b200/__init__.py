@@ -18,7 +18,7 @@ import torch
 from . import _lib
 from ._lib import HataError, Strides  # noqa: F401
 
-__all__ = ["hash_keys", "append", "decode_topk_attn", "decode_workspace_size", "decode_ranks",
+__all__ = ["hash_keys", "append", "decode_topk_attn", "decode_step", "decode_workspace_size", "decode_ranks",
            "shard_candidates", "shard_select", "shard_partial_attn", "shard_combine", "HataError", "lib"]
 
 
@@ -111,6 +111,31 @@ def decode_topk_attn(q, K, V, codes, W, n, k: int, n_max: int | None = None, sca
         _p(q.contiguous()), _p(K), _p(V), _strides4(K), _dt(K), _p(codes), _strides4(codes), _p(W), B, Hq, Hkv, d,
         rbits, _p(n), n_max, k, scale, _p(out), _dt(out), _p(out_idx), _p(out_score), _p(out_qcodes),
         _p(workspace) if ws else None, ws, _stream(stream)), "hata_decode_topk_attn")
+    return out
+
+
+def decode_step(q, k_new, v_new, K, V, codes, W, n, k: int, n_max: int | None = None, scale: float = 0.0,
+                out=None, out_dtype=torch.float32, out_idx=None, out_score=None, out_qcodes=None, workspace=None,
+                stream=None):
+    """Alg. 3 lines 2-17 in one launch: append k_new/v_new (and the key code) at
+    row n[b]-1, then decode.  ``n`` counts the new token.  Returns ``out``."""
+    _need_cuda(q, k_new, v_new, K, V, codes, W, n)
+    B, Hq, d = q.shape
+    Hkv, cap, rbits = K.shape[1], K.shape[2], W.shape[2]
+    if n_max is None:
+        n_max = cap
+    if out is None:
+        out = torch.empty(B, Hq, d, dtype=out_dtype, device=q.device)
+    if K.stride() != V.stride():
+        raise HataError("K and V must share strides")
+    ws = decode_workspace_size(B, Hq, Hkv, d, rbits, n_max, k, K.dtype)
+    if ws and (workspace is None or workspace.numel() * workspace.element_size() < ws):
+        workspace = torch.zeros(ws, dtype=torch.uint8, device=q.device)
+    _lib.check(lib().hata_decode_step(
+        _p(q.contiguous()), _p(k_new.contiguous()), _p(v_new.contiguous()), _p(K), _p(V), _strides4(K), _dt(K),
+        _p(codes), _strides4(codes), _p(W), B, Hq, Hkv, d, rbits, _p(n), n_max, cap, k, scale, _p(out), _dt(out),
+        _p(out_idx), _p(out_score), _p(out_qcodes), _p(workspace) if ws else None, ws, _stream(stream)),
+        "hata_decode_step")
     return out
 
 

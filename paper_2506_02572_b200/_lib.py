@@ -35,6 +35,9 @@ _SIGS = {
     "hata_decode_topk_attn": (c_i32, [c_ptr, c_ptr, c_ptr, Strides, c_i32, c_ptr, Strides, c_ptr, c_i32, c_i32,
                                       c_i32, c_i32, c_i32, c_ptr, c_i64, c_i32, c_f32, c_ptr, c_i32, c_ptr, c_ptr,
                                       c_ptr, c_ptr, c_size, c_ptr]),
+    "hata_decode_step": (c_i32, [c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, Strides, c_i32, c_ptr, Strides, c_ptr, c_i32,
+                                 c_i32, c_i32, c_i32, c_i32, c_ptr, c_i64, c_i64, c_i32, c_f32, c_ptr, c_i32, c_ptr,
+                                 c_ptr, c_ptr, c_ptr, c_size, c_ptr]),
     "hata_decode_workspace_size": (c_size, [c_i32, c_i32, c_i32, c_i32, c_i32, c_i64, c_i32, c_i32]),
     "hata_decode_ranks": (c_i32, [c_i32, c_i32, c_i32, c_i32, c_i32, c_i64, c_i32, c_i32]),
     "hata_shard_candidates": (c_i32, [c_ptr, c_i32, c_ptr, Strides, c_ptr, c_i32, c_i32, c_i32, c_i32, c_i32, c_ptr,
@@ -47,6 +50,7 @@ _SIGS = {
     "hata_status_string": (ctypes.c_char_p, [c_i32]),
     "hata_last_error": (ctypes.c_char_p, []),
     "hata_version": (ctypes.c_char_p, []),
+    "hata_debug_trace": (c_i32, [c_ptr]),
 }
 EXPORTS = tuple(_SIGS)
 

@@ -94,6 +94,8 @@ const char* hata_last_error(void) { return g_last_error; }
 
 const char* hata_version(void) { return "libhata 0.1 (sm_100a)"; }
 
+hata_status hata_debug_trace(void* buf) { return cuda_status(hata::set_decode_trace(buf)); }
+
 hata_status hata_hash_keys(const void* K, hata_strides ks, hata_dtype dt, const void* W, int B, int H_kv, int d,
                            int rbits, int64_t t0, int64_t n, uint32_t* codes, hata_strides cs,
                            hata_stream_t stream) {
@@ -149,7 +151,7 @@ static hata_status decode_common(const void* q, const void* K, const void* V, ha
                                  int d, int rbits, const int64_t* n, int64_t n_max, int k, float scale, void* out,
                                  hata_dtype out_dt, int32_t* out_idx, int32_t* out_score, uint32_t* out_qcodes,
                                  void* workspace, size_t ws_bytes, int cand_mode, int64_t token_offset,
-                                 int32_t* cand_D, hata_stream_t stream) {
+                                 int32_t* cand_D, const void* k_new, const void* v_new, hata_stream_t stream) {
   if (!q || !codes || !W || !n || B < 1 || H_kv < 1 || H_q < H_kv || H_q % H_kv || rbits < 32 || rbits % 32 ||
       n_max < 0 || k < 1 || !dtype_ok(dt))
     return HATA_ERR_INVALID_ARG;
@@ -171,6 +173,7 @@ static hata_status decode_common(const void* q, const void* K, const void* V, ha
   p.out = out; p.out_bf16 = out_dt == HATA_BF16;
   p.out_idx = out_idx; p.out_score = out_score; p.out_qcodes = out_qcodes;
   p.cand_mode = cand_mode; p.token_offset = token_offset; p.cand_D = cand_D;
+  p.k_new = k_new; p.v_new = v_new;
   return cuda_status(hata::launch_decode(p, pl, workspace, dt == HATA_BF16, reinterpret_cast<cudaStream_t>(stream)));
 }
 
@@ -180,7 +183,19 @@ hata_status hata_decode_topk_attn(const void* q, const void* K, const void* V, h
                                   hata_dtype out_dt, int32_t* out_idx, int32_t* out_score, uint32_t* out_qcodes,
                                   void* workspace, size_t ws_bytes, hata_stream_t stream) {
   return decode_common(q, K, V, kvs, dt, codes, cs, W, B, H_q, H_kv, d, rbits, n, n_max, k, scale, out, out_dt,
-                       out_idx, out_score, out_qcodes, workspace, ws_bytes, 0, 0, nullptr, stream);
+                       out_idx, out_score, out_qcodes, workspace, ws_bytes, 0, 0, nullptr, nullptr, nullptr, stream);
+}
+
+hata_status hata_decode_step(const void* q, const void* k_new, const void* v_new, void* K, void* V, hata_strides kvs,
+                             hata_dtype dt, uint32_t* codes, hata_strides cs, const void* W, int B, int H_q, int H_kv,
+                             int d, int rbits, const int64_t* n, int64_t n_max, int64_t cap, int k, float scale,
+                             void* out, hata_dtype out_dt, int32_t* out_idx, int32_t* out_score,
+                             uint32_t* out_qcodes, void* workspace, size_t ws_bytes, hata_stream_t stream) {
+  if (!k_new || !v_new) return HATA_ERR_INVALID_ARG;
+  if (n_max > cap) return HATA_ERR_CAPACITY;
+  if (!aligned(k_new, 16) || !aligned(v_new, 16)) return HATA_ERR_INVALID_ARG;
+  return decode_common(q, K, V, kvs, dt, codes, cs, W, B, H_q, H_kv, d, rbits, n, n_max, k, scale, out, out_dt,
+                       out_idx, out_score, out_qcodes, workspace, ws_bytes, 0, 0, nullptr, k_new, v_new, stream);
 }
 
 hata_status hata_shard_candidates(const void* q, hata_dtype dt, const uint32_t* codes, hata_strides cs,
@@ -192,7 +207,7 @@ hata_status hata_shard_candidates(const void* q, hata_dtype dt, const uint32_t* 
   hata_strides none = {0, 0, 0};
   return decode_common(q, nullptr, nullptr, none, dt, codes, cs, W, B, H_q, H_kv, d, rbits, n_local, n_local_max, k,
                        0.f, nullptr, HATA_F32, cand_idx, nullptr, nullptr, workspace, ws_bytes, 1, token_offset,
-                       cand_D, stream);
+                       cand_D, nullptr, nullptr, stream);
 }
 
 hata_status hata_shard_select(const int32_t* all_D, const int32_t* all_idx, int P, int B, int H_kv, int k, int G,

@@ -75,7 +75,7 @@ DecodePlan plan_decode(int B, int Hq, int Hkv, int d, int rbits, int64_t n_max, 
     if (v >= 1 && v <= DEC_MAX_RANKS && v * units <= sms) M = v;
   }
   const int region = DEC_RING_BYTES + ((d * rbits * eb + 127) & ~127);   // reusable after scoring
-  while (M > 1 && M * pl.nbins * 4 > region) --M;
+  while (M > 1 && M * dec_hist_stride(pl.nbins) * 4 > region) --M;
   pl.M = M;
   const int64_t per = (n_max + M - 1) / M;
   pl.chunk = (int)((per + DEC_CHUNK_ALIGN - 1) / DEC_CHUNK_ALIGN * DEC_CHUNK_ALIGN);
@@ -103,8 +103,8 @@ DecodePlan plan_decode(int B, int Hq, int Hkv, int d, int rbits, int64_t n_max, 
   // workspace (every section 256-byte aligned)
   size_t off = 0;
   pl.ws_sync = off;  off += M > 1 ? up256((size_t)units * 2 * 4) : 0;
-  pl.ws_hist = off;  off += M > 1 ? up256((size_t)units * M * pl.nbins * 4) : 0;
-  pl.ws_part = off;  off += M > 1 ? up256((size_t)units * M * GT * (d + 2) * 4) : 0;
+  pl.ws_hist = off;  off += M > 1 ? up256((size_t)units * M * dec_hist_stride(pl.nbins) * 4) : 0;
+  pl.ws_part = off;  off += M > 1 ? up256((size_t)units * M * dec_part_stride(GT, d) * 4) : 0;
   pl.ws_D = off;     off += (M > 1 || !pl.d_smem) ? up256((size_t)units * M * pl.chunk * 2) : 0;
   pl.ws_rows = off;  off += pl.rows_global ? up256((size_t)units * M * pl.R_cap * 4) : 0;
   pl.ws_total = off;
@@ -170,4 +170,11 @@ cudaError_t launch_partial_attn(PartialParams& p, int GT, int is_bf16, cudaStrea
   return cudaGetLastError();
 }
 
+}  // namespace hata
+
+namespace hata {
+cudaError_t set_decode_trace(void* buf) {
+  unsigned long long* p = reinterpret_cast<unsigned long long*>(buf);
+  return cudaMemcpyToSymbol(g_hata_trace, &p, sizeof(p));
+}
 }  // namespace hata

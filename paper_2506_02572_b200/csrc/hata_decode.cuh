@@ -20,7 +20,7 @@
 
 namespace hata {
 
-constexpr int DEC_THREADS = 256;
+constexpr int DEC_THREADS = 512;
 constexpr int DEC_WARPS = DEC_THREADS / 32;
 constexpr int DEC_STAGE_BYTES = 16384;       // one bulk copy of codes
 constexpr int DEC_STAGES = 6;                // code ring depth (96 KB in flight)
@@ -65,14 +65,38 @@ struct DecodeParams {
   int cand_mode;
   int64_t token_offset;    // global index of local token 0
   int32_t* cand_D;         // [B, Hkv, k] or null
+  // fused append (hata_decode_step): write k_new/v_new and the key code at row
+  // n[b]-1 before scoring; null = caches already hold the new token
+  const void* k_new;       // [B, Hkv, d]
+  const void* v_new;
 };
 
 struct DecodeSmem {
   int ring, W, bars, hist, D, qf, qw, planes, rows, red, misc, total;
+  int qp;                  // q-projection partial sums [DEC_THREADS/rbits][GT][rbits]
   int hm, kv, sc, rb;      // aliases inside ring+W after scoring
+  int sc_limit;            // end of the reusable ring+W area
 };
 
 __host__ __device__ inline int dec_qstride(int d) { return d + DEC_QS_PAD; }
+__host__ __device__ inline int dec_hist_stride(int nbins) { return (nbins + 3) & ~3; }
+// floats per rank partial block [GT][d+2], padded to 16 bytes
+__host__ __device__ inline int dec_part_stride(int GT, int d) { return (GT * (d + 2) + 3) & ~3; }
+
+// Diagnostics: when non-null, CTA (x, y) writes globaltimer stamps of its
+// phase boundaries to g_hata_trace[(y * gridDim.x + x) * 16 + i].  Set via
+// hata_debug_trace(); null (off) by default.  One copy per translation unit.
+static __device__ unsigned long long* g_hata_trace = nullptr;
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define HATA_TRACE(i)                                                                               \
+  do {                                                                                              \
+    if (g_hata_trace != nullptr && threadIdx.x == 0)                                                \
+      g_hata_trace[((size_t)blockIdx.y * gridDim.x + blockIdx.x) * 16 + (i)] = globaltimer_ns();    \
+  } while (0)
 
 // Shared-memory carve-up; identical on host and device.
 __host__ __device__ inline DecodeSmem decode_smem_layout(const DecodeParams& p, int GT, int eb) {
@@ -81,15 +105,16 @@ __host__ __device__ inline DecodeSmem decode_smem_layout(const DecodeParams& p, 
   int off = 0;
   s.ring = off; off += DEC_RING_BYTES;
   s.W = off; off += up(p.d * p.rbits * eb);
-  s.bars = off; off += up((DEC_STAGES + 2) * 8);
+  s.bars = off; off += up((DEC_STAGES + 3) * 8);
   s.hist = off; off += up(p.nbins * 4);
   s.D = off; off += p.d_smem ? up(p.chunk * 2) : 0;
-  s.qf = off; off += up(GT * dec_qstride(p.d) * 4);
-  s.qw = off; off += up(GT * (p.rbits / 32) * 4);
+  s.qf = off; off += up((GT + 1) * dec_qstride(p.d) * 4);
+  s.qw = off; off += up((GT + 1) * (p.rbits / 32) * 4);
   s.planes = off; off += up(2 * 4 * 8 * 4);
   s.rows = off; off += p.ws_rows ? 0 : up(p.R_cap * 4);
   s.red = off; off += up((DEC_MAX_RANKS * 4 + 64) * 4);
-  s.misc = off; off += up(64 * 4);
+  s.misc = off; off += up(128 * 4);   // [0,16) scalars, [16,80) warp counters, [80,104) softmax m/l/corr
+  s.qp = off; off += up(DEC_THREADS * (GT + 1) * 4);
   s.total = off;
   // after scoring the ring + W region is free:
   //   hm  : [M][nbins] int32 histograms of all ranks (select phase)
@@ -100,6 +125,7 @@ __host__ __device__ inline DecodeSmem decode_smem_layout(const DecodeParams& p, 
   s.kv = 0;
   s.sc = up(2 * p.rows_cap * rowb);
   s.rb = rowb;
+  s.sc_limit = s.bars;
   return s;
 }
 
@@ -119,22 +145,47 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 // below `quota`.  Each selected token gets position pos = base + #selected
 // before it in this chunk; positions in [P0, P1) are emitted via `emit`.
 // All threads of the block must call (block-uniform arguments).
+// Vectorised: a lane owns 8 consecutive tokens (one 16-byte load), a warp a
+// contiguous segment of 256-token blocks.  Dc must be 16-byte aligned.
 template <typename Emit>
 __device__ __forceinline__ void scan_chunk(const uint16_t* Dc, bool from_global, int L, int thr, int quota, int base,
                                            int P0, int P1, int* wcnt, Emit emit) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int seg = ((L + DEC_WARPS - 1) / DEC_WARPS + 31) & ~31;
+  const int seg = ((L + DEC_WARPS - 1) / DEC_WARPS + 255) & ~255;
   const int s0 = min(L, warp * seg), s1 = min(L, s0 + seg);
-  auto ldD = [&](int j) -> int {
-    if (j >= s1) return 0x7fffffff;
-    return from_global ? (int)__ldcg(Dc + j) : (int)Dc[j];
+  // 8-bit masks of (D < thr) and (D == thr) for tokens j .. j+7
+  auto masks = [&](int j, uint32_t& ltm, uint32_t& tim) {
+    uint32_t v[4];
+    if (j + 8 <= s1) {
+      const uint4 x = from_global ? __ldcg(reinterpret_cast<const uint4*>(Dc + j))
+                                  : *reinterpret_cast<const uint4*>(Dc + j);
+      v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
+    } else {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const uint32_t lo = (j + 2 * e < s1) ? (uint32_t)(from_global ? __ldcg(Dc + j + 2 * e) : Dc[j + 2 * e]) : 0xffffu;
+        const uint32_t hi = (j + 2 * e + 1 < s1) ? (uint32_t)(from_global ? __ldcg(Dc + j + 2 * e + 1) : Dc[j + 2 * e + 1])
+                                                 : 0xffffu;
+        v[e] = lo | (hi << 16);
+      }
+    }
+    ltm = 0; tim = 0;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int dv = (int)((v[e >> 1] >> (16 * (e & 1))) & 0xffffu);
+      ltm |= (uint32_t)(dv < thr) << e;
+      tim |= (uint32_t)(dv == thr) << e;
+    }
   };
   int lt_w = 0, ti_w = 0;
-  for (int j0 = s0; j0 < s1; j0 += 32) {
-    const int Dv = ldD(j0 + lane);
-    lt_w += __popc(__ballot_sync(0xffffffffu, Dv < thr));
-    ti_w += __popc(__ballot_sync(0xffffffffu, Dv == thr));
+  for (int j0 = s0; j0 < s1; j0 += 256) {
+    uint32_t ltm = 0, tim = 0;
+    if (j0 + 8 * lane < s1) masks(j0 + 8 * lane, ltm, tim);
+    lt_w += __popc(ltm);
+    ti_w += __popc(tim);
   }
+  lt_w = warp_sum_i(lt_w);
+  ti_w = warp_sum_i(ti_w);
   __syncthreads();                      // wcnt reuse guard
   if (lane == 0) { wcnt[2 * warp] = lt_w; wcnt[2 * warp + 1] = ti_w; }
   __syncthreads();
@@ -144,19 +195,37 @@ __device__ __forceinline__ void scan_chunk(const uint16_t* Dc, bool from_global,
   const int seg_first = base + lt_b + min(ti_b, quota);
   const int seg_last = base + lt_b + lt_w + min(ti_b + ti_w, quota);  // exclusive
   if (seg_last <= P0 || seg_first >= P1) return;
-  for (int j0 = s0; j0 < s1; j0 += 32) {
-    const int j = j0 + lane;
-    const int Dv = ldD(j);
-    const uint32_t lm = __ballot_sync(0xffffffffu, Dv < thr);
-    const uint32_t tm = __ballot_sync(0xffffffffu, Dv == thr);
-    const uint32_t below_me = (1u << lane) - 1u;
-    const int tr = ti_b + __popc(tm & below_me);
-    if (Dv < thr || (Dv == thr && tr < quota)) {
-      const int pos = base + lt_b + __popc(lm & below_me) + min(tr, quota);
-      if (pos >= P0 && pos < P1) emit(pos, j, Dv);
+  for (int j0 = s0; j0 < s1; j0 += 256) {
+    const int j = j0 + 8 * lane;
+    uint32_t ltm = 0, tim = 0;
+    if (j < s1) masks(j, ltm, tim);
+    // warp-exclusive prefix of (lt, tie) counts, packed in one int
+    const int mine = __popc(ltm) | (__popc(tim) << 16);
+    int incl = mine;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
     }
-    lt_b += __popc(lm);
-    ti_b += __popc(tm);
+    const int excl = incl - mine;
+    const int tot = __shfl_sync(0xffffffffu, incl, 31);
+    const int ltl = lt_b + (excl & 0xffff), til = ti_b + (excl >> 16);
+    uint32_t any = ltm | tim;
+    while (any) {
+      const int e = __ffs(any) - 1;
+      any &= any - 1;
+      const uint32_t below = (1u << e) - 1u;
+      const int tr = til + __popc(tim & below);
+      if (((ltm >> e) & 1u) || tr < quota) {
+        const int pos = base + ltl + __popc(ltm & below) + min(tr, quota);
+        if (pos >= P0 && pos < P1) {
+          const int dv = from_global ? (int)__ldcg(Dc + j + e) : (int)Dc[j + e];
+          emit(pos, j + e, dv);
+        }
+      }
+    }
+    lt_b += tot & 0xffff;
+    ti_b += tot >> 16;
   }
 }
 
@@ -191,13 +260,15 @@ __device__ __forceinline__ void attend_rows(const int32_t* rows, int Rr, const T
   for (int r0 = 0; r0 < Rr; r0 += rows_cap) {
     const int nb = min(rows_cap, Rr - r0);
     __syncthreads();                            // previous batch fully consumed
-    for (int c = tid; c < nb * CH * 2; c += DEC_THREADS) {
-      const int which = c / (nb * CH);          // 0: K, 1: V
-      const int rc = c - which * nb * CH;
-      const int i = rc / CH, ch = rc % CH;
-      const int64_t t = rows[r0 + i];
-      const T* src = (which ? Vb : Kb) + t * kv_st + ch * (16 / EB);
-      cp_async16((which ? Vs : Ks) + i * rowb + ch * 16, src);
+    {
+      // thread -> fixed (K|V, 16-byte chunk) column, strided over rows
+      constexpr int CH2 = 2 * CH;
+      static_assert(DEC_THREADS % CH2 == 0, "row stride");
+      const int col = tid % CH2, which = col / CH, ch = col % CH;
+      const T* base = (which ? Vb : Kb) + ch * (16 / EB);
+      uint8_t* dst = (which ? Vs : Ks) + ch * 16;
+      for (int i = tid / CH2; i < nb; i += DEC_THREADS / CH2)
+        cp_async16(dst + i * rowb, base + (int64_t)rows[r0 + i] * kv_st);
     }
     cp_async_wait_all();
     __syncthreads();
@@ -346,7 +417,8 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
 
   // ---- phase 0: start the code stream and the W_g copy (both q-independent)
   if (tid == 0) {
-    for (int s = 0; s < DEC_STAGES + 1; ++s) mbar_init(&bars[s], 1);
+    // code ring [0, STAGES), W copy [STAGES], histogram/D staging [STAGES + 1], partials [STAGES + 2]
+    for (int s = 0; s < DEC_STAGES + 3; ++s) mbar_init(&bars[s], 1);
     fence_mbar_init();
   }
   __syncthreads();
@@ -365,17 +437,73 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
   }
   for (int i = tid; i < p.nbins; i += DEC_THREADS) hist[i] = 0;
 
-  // ---- phase 1: hash the G query heads of the group (Alg. 3 line 6)
+  HATA_TRACE(0);
+  // ---- phase 1: Encode & Cache update (Alg. 3 lines 2-9; fused as
+  // in §4): hash the G query heads of the group and, when this launch
+  // also appends the new token (k_new != null), its key -- one projection pass
+  // with the key as row G.  The rank owning row pos = n-1 writes K/V/code rows.
+  const int64_t pos = n - 1;
+  const bool append = p.k_new != nullptr && n >= 1;
+  const bool owner = append && pos >= t0 && pos < t0 + Lr;
+  const int NV = G + (owner ? 1 : 0);                                // projected vectors
   const T* qg = reinterpret_cast<const T*>(p.q) + ((int64_t)b * p.Hq + (int64_t)g * G) * D_HEAD;
   for (int i = tid; i < G * D_HEAD; i += DEC_THREADS) qf[(i / D_HEAD) * QS + i % D_HEAD] = Elem<T>::to_f(qg[i]);
+  if (owner) {
+    const T* kn = reinterpret_cast<const T*>(p.k_new) + (int64_t)u * D_HEAD;
+    const T* vn = reinterpret_cast<const T*>(p.v_new) + (int64_t)u * D_HEAD;
+    T* Kd = const_cast<T*>(reinterpret_cast<const T*>(p.K)) + (int64_t)b * p.kv_sb + (int64_t)g * p.kv_sh + pos * p.kv_st;
+    T* Vd = const_cast<T*>(reinterpret_cast<const T*>(p.V)) + (int64_t)b * p.kv_sb + (int64_t)g * p.kv_sh + pos * p.kv_st;
+    for (int i = tid; i < D_HEAD; i += DEC_THREADS) {
+      const T kv = kn[i];
+      Kd[i] = kv;                                                      // Alg. 3 line 3
+      Vd[i] = vn[i];                                                   // Alg. 3 line 4
+      qf[G * QS + i] = Elem<T>::to_f(kv);
+    }
+  }
   __syncthreads();
   mbar_wait(&bars[DEC_STAGES], 0);
-  for (int wi = warp; wi < G * W; wi += DEC_WARPS) {
-    const int h = wi / W, w = wi % W;
-    const uint32_t word = hash_word_smem<T>(qf + h * QS, Ws, D_HEAD, p.rbits, w * 32, lane);
-    if (lane == 0) {
-      qw[h * W + w] = word;
-      if (p.out_qcodes && r == 0) p.out_qcodes[((int64_t)b * p.Hq + g * G + h) * W + w] = word;
+  {
+    // projection p[h][bit] = sum_j x_h[j] W[j][bit]: thread = (bit, j-slice), all
+    // vectors at once; slices summed in fixed order (fp32 accumulation, R13)
+    float* qpart = reinterpret_cast<float*>(smem + L.qp);           // [nparts][GT+1][rbits]
+    const int nparts = DEC_THREADS / p.rbits;
+    const int bit = tid % p.rbits, part = tid / p.rbits;           // part is warp-uniform
+    const int jlen = D_HEAD / nparts;
+    float acc[GT + 1];
+#pragma unroll
+    for (int h = 0; h <= GT; ++h) acc[h] = 0.f;
+    const T* wc = Ws + bit;
+    for (int j0 = part * jlen; j0 < (part + 1) * jlen; j0 += 4) {
+      float wv[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) wv[e] = Elem<T>::to_f(wc[(j0 + e) * p.rbits]);
+#pragma unroll
+      for (int h = 0; h <= GT; ++h) {
+        if (h < NV) {
+          const float4 qv = *reinterpret_cast<const float4*>(qf + h * QS + j0);
+          acc[h] = fmaf(qv.x, wv[0], acc[h]);
+          acc[h] = fmaf(qv.y, wv[1], acc[h]);
+          acc[h] = fmaf(qv.z, wv[2], acc[h]);
+          acc[h] = fmaf(qv.w, wv[3], acc[h]);
+        }
+      }
+    }
+#pragma unroll
+    for (int h = 0; h <= GT; ++h)
+      if (h < NV) qpart[(part * (GT + 1) + h) * p.rbits + bit] = acc[h];
+    __syncthreads();
+    // Sign + BitPack (Alg. 2 lines 5-7): a warp covers 32 consecutive bits of one vector
+    for (int o = tid; o < NV * p.rbits; o += DEC_THREADS) {
+      const int h = o / p.rbits, bb = o % p.rbits;
+      float sum = 0.f;
+      for (int pp = 0; pp < nparts; ++pp) sum += qpart[(pp * (GT + 1) + h) * p.rbits + bb];
+      const uint32_t word = __ballot_sync(0xffffffffu, sum >= 0.f);
+      if (lane == 0) {
+        qw[h * W + bb / 32] = word;                                    // row G = new key code
+        if (h < G && p.out_qcodes && r == 0) p.out_qcodes[((int64_t)b * p.Hq + g * G + h) * W + bb / 32] = word;
+        if (h == G)                                                    // Alg. 3 line 9
+          const_cast<uint32_t*>(p.codes)[(int64_t)b * p.c_sb + (int64_t)g * p.c_sh + pos * W + bb / 32] = word;
+      }
     }
   }
   __syncthreads();
@@ -398,6 +526,7 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
 #pragma unroll
     for (int w = 0; w < W; ++w) { A[j][w] = planes[j * 8 + w]; Bp[j][w] = planes[32 + j * 8 + w]; }
 
+  HATA_TRACE(1);
   // ---- phase 2: Hamming score + GQA sum (Alg. 3 lines 10-11) + histogram
   const bool mirror = (M > 1) && p.d_smem;          // D also needed by the other ranks
   for (int s = 0; s < nstages; ++s) {
@@ -446,16 +575,31 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
     __syncthreads();
     if (tid == 0 && s + DEC_STAGES < nstages) issue_stage(s + DEC_STAGES);
   }
+  if (owner && tid == 0) {
+    // the streamed row pos held the stale code: re-score the appended key
+    uint32_t kc[W];
+#pragma unroll
+    for (int w = 0; w < W; ++w) kc[w] = qw[G * W + w];
+    const int jl = (int)(pos - t0);
+    const uint32_t Dn = group_distance<W, J>(kc, A, Bp);
+    const uint32_t Do = Dloc[jl];
+    hist[Do] -= 1u;
+    hist[Dn] += 1u;
+    Dloc[jl] = (uint16_t)Dn;
+    if (mirror) Dglob[jl] = (uint16_t)Dn;
+  }
   __syncthreads();
 
   // ---- phase 3: exact top-k' (Alg. 3 lines 12-13) by counting select.
   // threshold thr = D of the k'-th best token; all D < thr are selected; ties
   // at thr are selected lowest index first (R8) via per-rank quotas in rank
   // (= token) order.  The ranks of a unit exchange histograms once.
-  int32_t* hm = reinterpret_cast<int32_t*>(smem + L.hm);           // [M][nbins]  (ring+W area)
+  const int hs = dec_hist_stride(p.nbins);                          // 16-byte rows
+  int32_t* hm = reinterpret_cast<int32_t*>(smem + L.hm);           // [M][hs]  (ring+W area)
   unsigned* sync = (M > 1) ? p.ws_sync + 2 * u : nullptr;
+  HATA_TRACE(2);
   if (M > 1) {
-    int32_t* gh = p.ws_hist + ((int64_t)u * M + r) * p.nbins;
+    int32_t* gh = p.ws_hist + ((int64_t)u * M + r) * hs;
     for (int i = tid; i < p.nbins; i += DEC_THREADS) gh[i] = (int32_t)hist[i];
     __syncthreads();
     if (tid == 0) {
@@ -463,18 +607,22 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
       atomicAdd(sync, 1u);
       while (ld_acquire_gpu(sync) < (unsigned)M) {
       }
+      // other ranks' generic-proxy writes -> this thread's async-proxy (bulk copy) reads
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+      const uint32_t bytes = (uint32_t)(M * hs * 4);
+      mbar_arrive_expect_tx(&bars[DEC_STAGES + 1], bytes);
+      bulk_g2s(hm, p.ws_hist + (int64_t)u * M * hs, bytes, &bars[DEC_STAGES + 1]);
     }
-    __syncthreads();
-    const int32_t* all = p.ws_hist + (int64_t)u * M * p.nbins;
-    for (int i = tid; i < M * p.nbins; i += DEC_THREADS) hm[i] = __ldcg(all + i);
+    mbar_wait(&bars[DEC_STAGES + 1], 0);
   } else {
     for (int i = tid; i < p.nbins; i += DEC_THREADS) hm[i] = (int32_t)hist[i];
+    __syncthreads();
   }
-  __syncthreads();
+  HATA_TRACE(3);
   // total histogram (reuse `hist`)
   for (int i = tid; i < p.nbins; i += DEC_THREADS) {
     int s = 0;
-    for (int rr = 0; rr < M; ++rr) s += hm[rr * p.nbins + i];
+    for (int rr = 0; rr < M; ++rr) s += hm[rr * hs + i];
     hist[i] = (uint32_t)s;
   }
   __syncthreads();
@@ -510,9 +658,9 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
   int32_t* rb_quota = red + 3 * DEC_MAX_RANKS;   // [M]
   for (int rr = warp; rr < M; rr += DEC_WARPS) {
     int s = 0;
-    for (int i = lane; i < thr; i += 32) s += hm[rr * p.nbins + i];
+    for (int i = lane; i < thr; i += 32) s += hm[rr * hs + i];
     s = warp_sum_i(s);
-    if (lane == 0) { rb_below[rr] = s; rb_ties[rr] = thr >= 0 ? hm[rr * p.nbins + thr] : 0; }
+    if (lane == 0) { rb_below[rr] = s; rb_ties[rr] = thr >= 0 ? hm[rr * hs + thr] : 0; }
   }
   __syncthreads();
   if (warp == 0) {
@@ -543,12 +691,44 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
   int32_t* ocd = p.cand_D ? p.cand_D + (int64_t)u * p.k : nullptr;
   const int Gr = G * p.rbits;
   int* wcnt = misc + 16;                         // [DEC_WARPS][2]
+  // stage the D arrays of the other ranks whose selections overlap [P0, P1)
+  // into smem with one bulk copy each (the ring + W area is free by now)
+  int32_t* dslot = red + 4 * DEC_MAX_RANKS;      // [M] smem byte offset of rank c's D copy, -1 if none
+  if (tid == 0) {
+    asm volatile("fence.proxy.async.global;" ::: "memory");   // D written by generic stores
+    uint32_t soff = (uint32_t)((M * hs * 4 + 127) & ~127), tx = 0;
+    for (int c = 0; c < M; ++c) {
+      dslot[c] = -1;
+      const int off = rb_off[c], cnt = rb_below[c] + rb_quota[c];
+      if (P1 <= P0 || cnt == 0 || off + cnt <= P0 || off >= P1) continue;
+      if (c == r && p.d_smem) continue;
+      const uint32_t bytes = (uint32_t)((chunk_len(c) * 2 + 15) & ~15);
+      if (soff + bytes > (uint32_t)L.sc_limit) continue;          // does not fit: scan from L2
+      dslot[c] = (int)soff;
+      tx += bytes;
+      soff += (bytes + 127) & ~127u;
+    }
+    if (tx) {
+      mbar_arrive_expect_tx(&bars[DEC_STAGES + 1], tx);
+      for (int c = 0; c < M; ++c)
+        if (dslot[c] >= 0)
+          bulk_g2s(smem + dslot[c], p.ws_D + ((int64_t)u * M + c) * p.chunk,
+                   (uint32_t)((chunk_len(c) * 2 + 15) & ~15), &bars[DEC_STAGES + 1]);
+    }
+    misc[3] = tx ? 1 : 0;
+  }
+  __syncthreads();
+  if (misc[3]) mbar_wait(&bars[DEC_STAGES + 1], M > 1 ? 1 : 0);
+  HATA_TRACE(4);
   for (int c = 0; c < M && P1 > P0; ++c) {
     const int off = rb_off[c], cnt = rb_below[c] + rb_quota[c];
     if (cnt == 0 || off + cnt <= P0 || off >= P1) continue;    // block-uniform
-    const bool own = (c == r);
-    const bool fromg = !(own && p.d_smem);
-    const uint16_t* Dc = fromg ? p.ws_D + ((int64_t)u * M + c) * p.chunk : Dloc;
+    const bool own = (c == r) && p.d_smem;
+    const bool staged = dslot[c] >= 0;
+    const bool fromg = !own && !staged;
+    const uint16_t* Dc = own ? Dloc
+                             : (staged ? reinterpret_cast<const uint16_t*>(smem + dslot[c])
+                                       : p.ws_D + ((int64_t)u * M + c) * p.chunk);
     const int64_t ctok = (int64_t)c * per;
     scan_chunk(Dc, fromg, chunk_len(c), thr, rb_quota[c], off, P0, P1, wcnt, [&](int pos, int j, int Dv) {
       const int tok = (int)(ctok + j);
@@ -567,10 +747,11 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
   }
   __syncthreads();
 
+  HATA_TRACE(5);
   // ---- phase 4: gather + softmax attention over this rank's rows (Alg. 3 lines 14-17)
-  float* m_s = fmisc + 32;
-  float* l_s = fmisc + 40;
-  float* corr_s = fmisc + 48;
+  float* m_s = fmisc + 80;
+  float* l_s = fmisc + 88;
+  float* corr_s = fmisc + 96;
   AttnState<GT, D_HEAD> st;
   if (!p.cand_mode) {
     const T* Kb = reinterpret_cast<const T*>(p.K) + (int64_t)b * p.kv_sb + (int64_t)g * p.kv_sh;
@@ -580,6 +761,7 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
                                m_s, l_s, corr_s, st);
   }
 
+  HATA_TRACE(6);
   // ---- phase 5: merge the M rank partials in rank order (flash-decoding combine)
   const int64_t orow = (int64_t)b * p.Hq + (int64_t)g * G;      // first output row of the group
   auto store_out = [&](int h, int e, float v) {
@@ -600,10 +782,11 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
         }
       }
     }
+    HATA_TRACE(7);
     return;
   }
   const int PS = D_HEAD + 2;
-  float* mypart = p.ws_part + ((int64_t)u * M + r) * GT * PS;
+  float* mypart = p.ws_part + ((int64_t)u * M + r) * dec_part_stride(GT, D_HEAD);
   if (!p.cand_mode) {
 #pragma unroll
     for (int s = 0; s < NSL; ++s) {
@@ -621,26 +804,36 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
   }
   __syncthreads();
   if (!misc[2]) return;
-  // last rank: all other partials are visible (their fence + the counter)
-  __threadfence();
+  // last rank: all other partials are visible (their fence + the counter);
+  // pull them into smem with one bulk copy, then merge in rank order
   if (!p.cand_mode) {
-    const float* parts = p.ws_part + (int64_t)u * M * GT * PS;
+    const int PB = dec_part_stride(GT, D_HEAD);
+    float* sp = reinterpret_cast<float*>(smem);                      // ring+W area is free
+    if (tid == 0) {
+      __threadfence();
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+      const uint32_t bytes = (uint32_t)(M * PB * 4);
+      mbar_arrive_expect_tx(&bars[DEC_STAGES + 2], bytes);
+      bulk_g2s(sp, p.ws_part + (int64_t)u * M * PB, bytes, &bars[DEC_STAGES + 2]);
+    }
+    mbar_wait(&bars[DEC_STAGES + 2], 0);
     for (int o = tid; o < G * D_HEAD; o += DEC_THREADS) {
       const int h = o / D_HEAD, e = o % D_HEAD;
       float Mx = -INFINITY;
-      for (int rr = 0; rr < M; ++rr) Mx = fmaxf(Mx, __ldcg(parts + (rr * GT + h) * PS));
+      for (int rr = 0; rr < M; ++rr) Mx = fmaxf(Mx, sp[rr * PB + h * PS]);
       float Ls = 0.f, As = 0.f;
       for (int rr = 0; rr < M; ++rr) {
-        const float* pr = parts + (rr * GT + h) * PS;
-        const float mr = __ldcg(pr);
+        const float* pr = sp + rr * PB + h * PS;
+        const float mr = pr[0];
         const float scl = (mr == -INFINITY) ? 0.f : expf(mr - Mx);
-        Ls = fmaf(__ldcg(pr + 1), scl, Ls);
-        As = fmaf(__ldcg(pr + 2 + e), scl, As);
+        Ls = fmaf(pr[1], scl, Ls);
+        As = fmaf(pr[2 + e], scl, As);
       }
       store_out(h, e, Ls > 0.f ? As / Ls : 0.f);
     }
   }
   if (tid == 0) { sync[0] = 0u; sync[1] = 0u; }     // leave the workspace zeroed for the next launch
+  HATA_TRACE(7);
 }
 
 // ---------------------------------------------------------------------------

@@ -65,3 +65,7 @@ cudaError_t launch_partial_attn(PartialParams& p, int GT, int is_bf16, cudaStrea
 int device_sm_count();
 
 }  // namespace hata
+
+namespace hata {
+cudaError_t set_decode_trace(void* buf);
+}  // namespace hata

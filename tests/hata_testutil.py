@@ -18,8 +18,9 @@ def codes_u32(t: torch.Tensor) -> np.ndarray:
     return t.detach().cpu().numpy().view(np.uint32)
 
 
-def gpu_step(case: dict, k: int, n_override=None, out_dtype=torch.float32, device="cuda"):
-    """prefill-hash rows [0, N-1), append row n_before, decode; all via the C ABI."""
+def gpu_step(case: dict, k: int, n_override=None, out_dtype=torch.float32, device="cuda", fused=False):
+    """prefill-hash rows [0, N-1), append row n_before, decode; all via the C ABI.
+    fused=True runs append + decode as one hata_decode_step launch."""
     import paper_2506_02572_b200 as H
     sh = case["shape"]
     q = case["q"].to(device)
@@ -32,14 +33,18 @@ def gpu_step(case: dict, k: int, n_override=None, out_dtype=torch.float32, devic
     Wd = sh.rbits // 32
     codes = torch.zeros(B, Hkv, cap, Wd, dtype=torch.int32, device=device)
     H.hash_keys(K, W, codes, 0, int(nb.max().item()))
-    H.append(kn, vn, W, K, V, codes, nb)
     n = nb + 1
     n_max = int(n.max().item())
     out_idx = torch.full((B, Hkv, k), -7, dtype=torch.int32, device=device)
     out_score = torch.zeros(B, Hkv, k, dtype=torch.int32, device=device)
     qcodes = torch.zeros(B, sh.Hq, Wd, dtype=torch.int32, device=device)
-    out = H.decode_topk_attn(q, K, V, codes, W, n, k, n_max=n_max, out_dtype=out_dtype, out_idx=out_idx,
-                             out_score=out_score, out_qcodes=qcodes)
+    if fused:
+        out = H.decode_step(q, kn, vn, K, V, codes, W, n, k, n_max=n_max, out_dtype=out_dtype, out_idx=out_idx,
+                            out_score=out_score, out_qcodes=qcodes)
+    else:
+        H.append(kn, vn, W, K, V, codes, nb)
+        out = H.decode_topk_attn(q, K, V, codes, W, n, k, n_max=n_max, out_dtype=out_dtype, out_idx=out_idx,
+                                 out_score=out_score, out_qcodes=qcodes)
     torch.cuda.synchronize()
     return dict(K=K.cpu(), V=V.cpu(), codes=codes.cpu(), out=out.cpu(), idx=out_idx.cpu(),
                 score=out_score.cpu(), qc=qcodes.cpu(), n=n.cpu())

@@ -35,20 +35,21 @@ SMALL = [
 
 
 @pytest.mark.parametrize("name,shape,variant", SMALL, ids=[s[0] for s in SMALL])
-def test_decode_parity_small(name, shape, variant):
+@pytest.mark.parametrize("fused", [False, True], ids=["append+decode", "decode_step"])
+def test_decode_parity_small(name, shape, variant, fused):
     case = synth.make_case(shape, seed=11, variant=variant)
-    g = gpu_step(case, shape.k)
+    g = gpu_step(case, shape.k, fused=fused)
     st = check_decode(case, g, shape.k)
     print(name, st)
 
 
-def test_decode_parity_ragged_batch():
+@pytest.mark.parametrize("fused", [False, True], ids=["append+decode", "decode_step"])
+def test_decode_parity_ragged_batch(fused):
     shape = _shape("cfg2", B=3, N=6000, k=400)
     case = synth.make_case(shape, seed=5, cap=6000)
     nb = torch.tensor([5999, 4000, 17], dtype=torch.int64)
     case["n_before"] = nb
-    # append rows at n_before: take the new k/v from those rows of the generator's K/V
-    g = gpu_step(case, shape.k, n_override=nb)
+    g = gpu_step(case, shape.k, n_override=nb, fused=fused)
     st = check_decode(case, g, shape.k)
     print(st)
 
@@ -58,7 +59,7 @@ def test_decode_parity_full_size(name):
     """BASELINE sizes, bench launch configuration; codes sampled per head."""
     shape = synth.CONFIGS[name]
     case = synth.make_case(shape, seed=1)
-    g = gpu_step(case, shape.k)
+    g = gpu_step(case, shape.k, fused=True)     # the launch bench.py times
     st = check_decode(case, g, shape.k, code_rows_sample=65536)
     print(name, st)
 

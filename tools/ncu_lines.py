@@ -61,7 +61,8 @@ def main():
         ex[key] += float(r[i_x] or 0)
         tot += s
     srcfiles = {}
-    for (f, ln), s in agg.most_common(top):
+    order = agg.most_common(top) if os.environ.get("SORT") != "inst" else [(k2, agg[k2]) for k2, _ in ex.most_common(top)]
+    for (f, ln), s in order:
         text = ""
         for cand in glob.glob(os.path.join(os.path.dirname(__file__), "..", "paper_2506_02572_b200", "csrc", f)):
             srcfiles.setdefault(cand, open(cand).read().splitlines())
