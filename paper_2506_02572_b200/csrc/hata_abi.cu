@@ -168,7 +168,7 @@ static hata_status decode_common(const void* q, const void* K, const void* V, ha
   hata::DecodeParams p = {};
   p.q = q; p.K = K; p.V = V; p.kv_sb = kvs.sb; p.kv_sh = kvs.sh; p.kv_st = kvs.st;
   p.codes = codes; p.c_sb = cs.sb; p.c_sh = cs.sh; p.Wh = W; p.n = n;
-  p.B = B; p.Hq = H_q; p.Hkv = H_kv; p.G = H_q / H_kv; p.d = d; p.rbits = rbits; p.k = k;
+  p.B = B; p.Hq = H_q; p.Hkv = H_kv; p.G = H_q / H_kv; p.d = d; p.rbits = rbits; p.k = k; p.n_max = n_max;
   p.scale = scale != 0.f ? scale : 1.0f / sqrtf((float)d);
   p.out = out; p.out_bf16 = out_dt == HATA_BF16;
   p.out_idx = out_idx; p.out_score = out_score; p.out_qcodes = out_qcodes;

@@ -1,7 +1,7 @@
 // Host-side planning + dispatch of the fused decode kernel (hata_decode.cuh).
 #include <cstdlib>
 #include "hata_internal.h"
-#include "hata_decode.cuh"
+#include "hata_decode_kernel.cuh"
 
 namespace hata {
 
@@ -74,31 +74,50 @@ DecodePlan plan_decode(int B, int Hq, int Hkv, int d, int rbits, int64_t n_max, 
     const int v = std::atoi(e);
     if (v >= 1 && v <= DEC_MAX_RANKS && v * units <= sms) M = v;
   }
-  const int region = DEC_RING_BYTES + ((d * rbits * eb + 127) & ~127);   // reusable after scoring
-  while (M > 1 && M * dec_hist_stride(pl.nbins) * 4 > region) --M;
-  pl.M = M;
-  const int64_t per = (n_max + M - 1) / M;
-  pl.chunk = (int)((per + DEC_CHUNK_ALIGN - 1) / DEC_CHUNK_ALIGN * DEC_CHUNK_ALIGN);
-  if (pl.chunk < DEC_CHUNK_ALIGN) pl.chunk = DEC_CHUNK_ALIGN;
-  const int64_t kmax = k < n_max ? k : n_max;
-  pl.R_cap = (int)((kmax + M - 1) / M);
-  if (pl.R_cap < 1) pl.R_cap = 1;
-  pl.rows_global = pl.R_cap > ROWS_SMEM_MAX;
   const int rowb = d * eb + DEC_ROW_PAD;
-  int rc = region / (2 * rowb + GT * 4) - 1;
-  if (rc > pl.R_cap) rc = pl.R_cap;
-  if (rc < 1) rc = 1;
-  pl.rows_cap = rc;
-  // D in smem if the whole layout still fits
-  DecodeParams sp = {};
-  sp.d = d; sp.rbits = rbits; sp.nbins = pl.nbins; sp.chunk = pl.chunk; sp.rows_cap = pl.rows_cap;
-  sp.R_cap = pl.R_cap; sp.ws_rows = pl.rows_global ? reinterpret_cast<int32_t*>(256) : nullptr;
-  sp.d_smem = 1;
-  pl.smem = decode_smem_layout(sp, GT, eb).total;
-  pl.d_smem = pl.smem <= SMEM_LIMIT;
-  if (!pl.d_smem) {
-    sp.d_smem = 0;
-    pl.smem = decode_smem_layout(sp, GT, eb).total;
+  const int wbytes = (d * rbits * eb + 127) & ~127;
+  for (;;) {
+    pl.M = M;
+    const int64_t per = (n_max + M - 1) / M;
+    pl.chunk = (int)((per + DEC_CHUNK_ALIGN - 1) / DEC_CHUNK_ALIGN * DEC_CHUNK_ALIGN);
+    if (pl.chunk < DEC_CHUNK_ALIGN) pl.chunk = DEC_CHUNK_ALIGN;
+    const int64_t kmax = k < n_max ? k : n_max;
+    pl.R_cap = (int)((kmax + M - 1) / M);
+    if (pl.R_cap < 1) pl.R_cap = 1;
+    pl.rows_global = pl.R_cap > ROWS_SMEM_MAX;
+    // shared memory: the code ring holds the whole chunk when it can (8 x 16 KB);
+    // prefer keeping D on chip over a deep ring (shrink to 4 stages first)
+    DecodeParams sp = {};
+    sp.d = d; sp.rbits = rbits; sp.nbins = pl.nbins; sp.chunk = pl.chunk; sp.rows_cap = 1;
+    sp.R_cap = pl.R_cap; sp.ws_rows = pl.rows_global ? reinterpret_cast<int32_t*>(256) : nullptr;
+    sp.d_smem = 1;
+    pl.stages = DEC_MAX_STAGES;
+    for (;; --pl.stages) {
+      sp.stages = pl.stages;
+      pl.smem = decode_smem_layout(sp, GT, eb).total;
+      if (pl.smem <= SMEM_LIMIT || pl.stages == 4) break;
+    }
+    pl.d_smem = pl.smem <= SMEM_LIMIT;
+    if (!pl.d_smem) {
+      sp.d_smem = 0;
+      pl.stages = DEC_MAX_STAGES;
+      for (;; --pl.stages) {
+        sp.stages = pl.stages;
+        pl.smem = decode_smem_layout(sp, GT, eb).total;
+        if (pl.smem <= SMEM_LIMIT || pl.stages == 2) break;
+      }
+    }
+    // the ring + W area is reused after scoring: histograms of all ranks, the
+    // staged K/V rows of one attention batch, the partials of all ranks
+    const int region = pl.stages * DEC_STAGE_BYTES + wbytes;
+    int rc = region / (2 * rowb + GT * 4) - 1;
+    if (rc > pl.R_cap) rc = pl.R_cap;
+    if (rc < 1) rc = 1;
+    pl.rows_cap = rc;
+    const bool fits = M * dec_hist_stride(pl.nbins) * 4 + 128 <= region &&
+                      M * (dec_part_stride(GT, d) + GT) * 4 + 256 <= region;
+    if (fits || M == 1) break;
+    --M;
   }
   // workspace (every section 256-byte aligned)
   size_t off = 0;
@@ -115,7 +134,8 @@ cudaError_t launch_decode(DecodeParams& p, const DecodePlan& pl, void* ws, int i
   DecodeKernel kern = get_kernel(is_bf16, p.rbits / 32, pl.GT);
   if (!kern) return cudaErrorNotSupported;
   uint8_t* w = reinterpret_cast<uint8_t*>(ws);
-  p.M = pl.M; p.chunk = pl.chunk; p.nbins = pl.nbins; p.rows_cap = pl.rows_cap; p.R_cap = pl.R_cap;
+  p.trace = decode_trace_buf();
+  p.M = pl.M; p.stages = pl.stages; p.chunk = pl.chunk; p.nbins = pl.nbins; p.rows_cap = pl.rows_cap; p.R_cap = pl.R_cap;
   p.d_smem = pl.d_smem;
   p.ws_sync = pl.M > 1 ? reinterpret_cast<unsigned*>(w + pl.ws_sync) : nullptr;
   p.ws_hist = pl.M > 1 ? reinterpret_cast<int32_t*>(w + pl.ws_hist) : nullptr;
@@ -173,8 +193,10 @@ cudaError_t launch_partial_attn(PartialParams& p, int GT, int is_bf16, cudaStrea
 }  // namespace hata
 
 namespace hata {
+static unsigned long long* g_trace_buf = nullptr;   // host-side: copied into DecodeParams::trace
 cudaError_t set_decode_trace(void* buf) {
-  unsigned long long* p = reinterpret_cast<unsigned long long*>(buf);
-  return cudaMemcpyToSymbol(g_hata_trace, &p, sizeof(p));
+  g_trace_buf = reinterpret_cast<unsigned long long*>(buf);
+  return cudaSuccess;
 }
+unsigned long long* decode_trace_buf() { return g_trace_buf; }
 }  // namespace hata

@@ -36,7 +36,7 @@ cudaError_t launch_hash_keys_simt(const HashKeysParams& p, int is_bf16, cudaStre
 cudaError_t launch_hash_keys_tc(const HashKeysParams& p, cudaStream_t s);
 
 struct DecodePlan {
-  int M, chunk, R_cap, rows_cap, nbins, GT, smem;
+  int M, stages, chunk, R_cap, rows_cap, nbins, GT, smem;
   bool d_smem, rows_global;
   size_t ws_sync, ws_hist, ws_part, ws_D, ws_rows, ws_total;   // workspace byte offsets / size
 };
@@ -68,4 +68,7 @@ int device_sm_count();
 
 namespace hata {
 cudaError_t set_decode_trace(void* buf);
+}  // namespace hata
+namespace hata {
+unsigned long long* decode_trace_buf();
 }  // namespace hata

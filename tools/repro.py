@@ -23,9 +23,10 @@ def main():
     rb = int(a[5]) if len(a) > 5 else 128
     dt = a[6] if len(a) > 6 else "bf16"
     var = a[7] if len(a) > 7 else "planted"
+    fused = (a[8] == "1") if len(a) > 8 else True
     sh = dataclasses.replace(synth.CONFIGS["cfg2"], N=N, k=k, B=B, Hq=Hq, Hkv=Hkv, rbits=rb, dtype=dt)
     case = synth.make_case(sh, 11, variant=var)
-    g = gpu_step(case, k)
+    g = gpu_step(case, k, fused=fused)
     print(check_decode(case, g, k))
 
 

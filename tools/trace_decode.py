@@ -1,8 +1,8 @@
 """Per-phase timeline of the fused decode kernel (dev tool, needs a GPU).
 
-python tools/trace_decode.py [cfg4] [reps]
-Prints, per phase boundary, the median / max over CTAs of (stamp - kernel start)
-in microseconds, using hata_debug_trace() (%globaltimer stamps).
+python tools/trace_decode.py [cfg4] [reps] [fused(1)|unfused(0)]
+Prints, per stamp, the median / max over CTAs of (stamp - kernel start) in
+microseconds (hata_debug_trace(), %globaltimer), stamps sorted by median.
 """
 import os
 import sys
@@ -15,12 +15,15 @@ import torch  # noqa: E402
 import bench  # noqa: E402
 import synth  # noqa: E402
 
-NAMES = ["start", "qhash", "score", "hist_x", "D_staged", "select", "attn", "end"]
+NAMES = {0: "start", 1: "hash_done", 2: "score_done", 3: "hist_x", 4: "D_staged", 5: "select_done",
+         6: "attn_done", 7: "end(last)", 8: "qk_loaded", 9: "W_ready", 10: "stage0", 11: "thr",
+         12: "quota", 13: "stage_issued", 14: "kv_gathered", 15: "published"}
 
 
 def main():
     cfg = sys.argv[1] if len(sys.argv) > 1 else "cfg4"
-    reps = int(sys.argv[2]) if len(sys.argv) > 2 else 5
+    reps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
+    fused = (sys.argv[3] != "0") if len(sys.argv) > 3 else True
     sh = synth.CONFIGS[cfg]
     dev = torch.device("cuda", 0)
     sets = [bench.Step(sh, 2000 + i, dev) for i in range(8)]
@@ -32,24 +35,24 @@ def main():
         s.run()
     torch.cuda.synchronize()
     H._lib.check(H.lib().hata_debug_trace(buf.data_ptr()), "trace")
-    rows = []
+    print(f"{cfg}: M={M} ranks x {sh.B * sh.Hkv} units = {nct} CTAs  ({'fused' if fused else 'decode only'})")
     for rep in range(reps):
         s = sets[rep % len(sets)]
         buf.zero_()
-        s.decode()
+        (s.run if fused else s.decode)()
         torch.cuda.synchronize()
-        t = buf.view(nct, 16)[:, :8].cpu().double()
-        t0 = t[:, 0].min()
-        rows.append((t - t0) / 1e3)
+        t = buf.view(nct, 16).cpu().double()
+        t0 = t[:, 0][t[:, 0] > 0].min()
+        cols = []
+        for i in range(16):
+            c = t[:, i]
+            c = c[c > 0]
+            if len(c):
+                c = (c - t0) / 1e3
+                cols.append((c.median().item(), c.max().item(), NAMES[i]))
+        cols.sort()
+        print(f"rep{rep} " + " ".join(f"{nm}={md:.2f}/{mx:.2f}" for md, mx, nm in cols))
     H._lib.check(H.lib().hata_debug_trace(None), "trace off")
-    print(f"{cfg}: M={M} ranks x {sh.B * sh.Hkv} units = {nct} CTAs")
-    for rep, t in enumerate(rows):
-        valid = t[:, 7] > 0
-        parts = []
-        for i, nm in enumerate(NAMES):
-            col = t[:, i][t[:, i] >= 0]
-            parts.append(f"{nm}={col.median().item():6.2f}/{col.max().item():6.2f}")
-        print(f"rep{rep} " + " ".join(parts))
 
 
 if __name__ == "__main__":
