@@ -219,6 +219,9 @@ const char* hata_version(void);
  * (0 start, 1 q-hash done, 2 score done, 3 histograms exchanged, 4 D staged,
  * 5 selection done, 6 attention done, 7 end).  Not for production use. */
 hata_status hata_debug_trace(void* buf);
+/* Diagnostics only: enqueue a 1-thread kernel that stores %globaltimer (ns)
+ * to *dst (device uint64), to bracket a traced launch on the same stream. */
+hata_status hata_debug_timestamp(void* dst, hata_stream_t stream);
 
 #ifdef __cplusplus
 }

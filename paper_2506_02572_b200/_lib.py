@@ -51,6 +51,7 @@ _SIGS = {
     "hata_last_error": (ctypes.c_char_p, []),
     "hata_version": (ctypes.c_char_p, []),
     "hata_debug_trace": (c_i32, [c_ptr]),
+    "hata_debug_timestamp": (c_i32, [c_ptr, c_ptr]),
 }
 EXPORTS = tuple(_SIGS)
 

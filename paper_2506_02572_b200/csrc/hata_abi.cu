@@ -96,6 +96,11 @@ const char* hata_version(void) { return "libhata 0.1 (sm_100a)"; }
 
 hata_status hata_debug_trace(void* buf) { return cuda_status(hata::set_decode_trace(buf)); }
 
+hata_status hata_debug_timestamp(void* dst, hata_stream_t stream) {
+  if (!dst) return HATA_ERR_INVALID_ARG;
+  return cuda_status(hata::launch_timestamp(dst, reinterpret_cast<cudaStream_t>(stream)));
+}
+
 hata_status hata_hash_keys(const void* K, hata_strides ks, hata_dtype dt, const void* W, int B, int H_kv, int d,
                            int rbits, int64_t t0, int64_t n, uint32_t* codes, hata_strides cs,
                            hata_stream_t stream) {

@@ -1,0 +1,187 @@
+// Gather-fused sparse attention on the tensor cores (bf16 K/V; mma.sync
+// m16n8k16, fp32 accumulation).  Alg. 3 lines 14-17 with the
+// gather fused into the attention: the selected K/V rows are staged
+// in smem by cp.async and never materialised in HBM.
+//
+// Per batch of staged rows, warp w takes 16-row groups w, w + NW, ...:
+//   S  = Q . K_g^T           Q: the G heads of the group as A (rows >= G zero)
+//   online softmax per warp  (running max m, sum l per head, fp32)
+//   O += P . V_g             P split into bf16 hi + lo (two MMAs) so that the
+//                            probabilities keep ~16 mantissa bits (R14)
+// Afterwards the warps' (m, l, O) are merged in fixed warp order into the
+// CTA partial: m_s[h], l_s[h] and st.acc (the same layout attend_rows gives).
+#pragma once
+#include "hata_decode.cuh"
+
+namespace hata {
+
+template <int GT, int D_HEAD>
+__device__ __forceinline__ void attend_rows_mma(const int32_t* rows, int Rr, const __nv_bfloat16* __restrict__ Kb,
+                                                const __nv_bfloat16* __restrict__ Vb, int64_t kv_st, const float* qf,
+                                                int G, float scale, uint8_t* kvbuf, int rows_cap, int rowb,
+                                                float* m_s, float* l_s, AttnState<GT, D_HEAD>& st,
+                                                uint64_t* bar, unsigned long long* tr = nullptr, int tb = 16) {
+  static_assert(GT <= 8, "heads per group <= 8");
+  constexpr int CH = D_HEAD * 2 / 16;            // 16-byte chunks per row
+  constexpr int KS = D_HEAD / 16;                // k-steps over the head dim
+  constexpr int NT = D_HEAD / 8;                 // output column tiles
+  constexpr int NSL = AttnState<GT, D_HEAD>::NSL;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int gid = lane >> 2, tig = lane & 3;
+  const int QS = dec_qstride(D_HEAD);
+  uint8_t* Ks = kvbuf;
+  uint8_t* Vs = kvbuf + rows_cap * rowb;
+
+  // Q as A fragments (exact: q is bf16), built per k-step from smem; heads
+  // >= G and rows 8..15 are zero
+  const float* qrow = qf + (gid < G ? gid : 0) * QS + 2 * tig;
+  const bool qvalid = gid < G;
+  float O[NT][4];
+#pragma unroll
+  for (int t = 0; t < NT; ++t) O[t][0] = O[t][1] = O[t][2] = O[t][3] = 0.f;
+  float m_run = -INFINITY, l_run = 0.f;          // head gid, this warp
+  bool active = false;
+
+  uint32_t bpar = 0;
+  for (int r0 = 0; r0 < Rr; r0 += rows_cap) {
+    const int nb = min(rows_cap, Rr - r0);
+    __syncthreads();                             // previous batch fully consumed
+    // gather: one bulk copy per selected K or V row (TMA engine, no per-16B
+    // requests in the LSU), all on one mbarrier
+    constexpr uint32_t ROWBYTES = D_HEAD * 2;
+    if (tid == 0) mbar_arrive_expect_tx(bar, 2u * ROWBYTES * (uint32_t)nb);
+    __syncthreads();
+    if (r0 == 0) trace_at(tr, tb + 4);
+    // request i -> warp i % NW, lane i / NW: a warp issues its bulk copies one
+    // lane after another, so spread them over all warps
+    for (int i = lane * DEC_WARPS + warp; i < 2 * nb; i += DEC_THREADS) {
+      const int which = i >= nb, rr = i - (which ? nb : 0);
+      const __nv_bfloat16* src = (which ? Vb : Kb) + (int64_t)rows[r0 + rr] * kv_st;
+      bulk_g2s((which ? Vs : Ks) + rr * rowb, src, ROWBYTES, bar);
+    }
+    if (r0 == 0) trace_at(tr, tb + 3);
+    mbar_wait(bar, bpar);
+    bpar ^= 1u;
+    if (r0 == 0) trace_at(tr, tb);
+    for (int g0 = warp * 16; g0 < nb; g0 += DEC_WARPS * 16) {
+      active = true;
+      // S = Q K^T for rows g0 .. g0+15 (two 8-row tiles)
+      float S[2][4];
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+        S[t][0] = S[t][1] = S[t][2] = S[t][3] = 0.f;
+        int row = g0 + 8 * t + gid;
+        row = row < nb ? row : g0;                                   // padded rows: any valid data
+        const uint8_t* kr = Ks + row * rowb + 4 * tig;
+#pragma unroll
+        for (int ks = 0; ks < KS; ++ks) {
+          const uint32_t b0 = *reinterpret_cast<const uint32_t*>(kr + ks * 32);
+          const uint32_t b1 = *reinterpret_cast<const uint32_t*>(kr + ks * 32 + 16);
+          const float2 f0 = *reinterpret_cast<const float2*>(qrow + ks * 16);
+          const float2 f2 = *reinterpret_cast<const float2*>(qrow + ks * 16 + 8);
+          const uint32_t a[4] = {qvalid ? pack_bf16x2(f0.x, f0.y) : 0u, 0u, qvalid ? pack_bf16x2(f2.x, f2.y) : 0u, 0u};
+          mma_bf16_16816(S[t], a, b0, b1);
+        }
+      }
+      // head gid owns S[t][0..1] = rows g0 + 8t + 2tig, +1
+      float z[4];
+#pragma unroll
+      for (int t = 0; t < 2; ++t)
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          const int row = g0 + 8 * t + 2 * tig + c;
+          z[2 * t + c] = row < nb ? S[t][c] * scale : -INFINITY;
+        }
+      float mx = fmaxf(fmaxf(z[0], z[1]), fmaxf(z[2], z[3]));
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+      const float mn = fmaxf(m_run, mx);
+      const float corr = (m_run == -INFINITY) ? 0.f : expf(m_run - mn);
+      float pz[4], ps = 0.f;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) { pz[i] = expf(z[i] - mn); ps += pz[i]; }
+      ps += __shfl_xor_sync(0xffffffffu, ps, 1);
+      ps += __shfl_xor_sync(0xffffffffu, ps, 2);
+      l_run = l_run * corr + ps;
+      m_run = mn;
+#pragma unroll
+      for (int t = 0; t < NT; ++t) { O[t][0] *= corr; O[t][1] *= corr; O[t][2] *= corr; O[t][3] *= corr; }
+      // P as the A fragment (k = the 16 rows): rows 0-7 carry bf16(p) of the
+      // heads, rows 8-15 the residual p - bf16(p), so one MMA yields both
+      // halves (c0,c1: hi, c2,c3: lo; summed at the end)
+      uint32_t pa[4];
+      {
+        const __nv_bfloat162 h0 = __floats2bfloat162_rn(pz[0], pz[1]);
+        const __nv_bfloat162 h2 = __floats2bfloat162_rn(pz[2], pz[3]);
+        const float2 b0f = __bfloat1622float2(h0), b2f = __bfloat1622float2(h2);
+        pa[0] = *reinterpret_cast<const uint32_t*>(&h0);
+        pa[2] = *reinterpret_cast<const uint32_t*>(&h2);
+        pa[1] = pack_bf16x2(pz[0] - b0f.x, pz[1] - b0f.y);
+        pa[3] = pack_bf16x2(pz[2] - b2f.x, pz[3] - b2f.y);
+      }
+      // O += P V over the 16 rows; V rows via ldmatrix.trans (padded rows)
+      int vrow = g0 + (lane & 15);
+      vrow = vrow < nb ? vrow : g0;
+      const uint8_t* vr = Vs + vrow * rowb;
+#pragma unroll
+      for (int t = 0; t < NT; ++t) {
+        uint32_t b0, b1;
+        ldsm_x2_trans(b0, b1, vr + t * 16);
+        mma_bf16_16816(O[t], pa, b0, b1);
+      }
+    }
+  }
+  // merge the warps in fixed order: smem [warp][GT][D_HEAD + 2] over the K/V area
+  __syncthreads();
+  trace_at(tr, tb + 1);
+  float* wp = reinterpret_cast<float*>(kvbuf);
+  const int PS = D_HEAD + 2;
+  if (gid < G) {
+    float* dst = wp + (warp * GT + gid) * PS;
+    if (tig == 0) { dst[0] = active ? m_run : -INFINITY; dst[1] = active ? l_run : 0.f; }
+#pragma unroll
+    for (int t = 0; t < NT; ++t) {
+      dst[2 + t * 8 + 2 * tig] = O[t][0] + O[t][2];                // hi + lo halves of P
+      dst[2 + t * 8 + 2 * tig + 1] = O[t][1] + O[t][3];
+    }
+  }
+  // only the first nact warps ever held rows
+  const int nact = min(DEC_WARPS, (min(Rr, rows_cap) + 15) / 16);
+  float* wgt = wp + DEC_WARPS * GT * PS;                            // [DEC_WARPS][GT] merge weights
+  __syncthreads();
+  // per head: max over warps (one warp per head, lanes = warps)
+  if (warp < G) {
+    const float mw = lane < nact ? wp[(lane * GT + warp) * PS] : -INFINITY;
+    float Mx = mw;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) Mx = fmaxf(Mx, __shfl_xor_sync(0xffffffffu, Mx, o));
+    const float wv = (mw == -INFINITY) ? 0.f : expf(mw - Mx);
+    const float lw = lane < nact ? wp[(lane * GT + warp) * PS + 1] * wv : 0.f;
+    float L = lw;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) L += __shfl_xor_sync(0xffffffffu, L, o);
+    if (lane < DEC_WARPS) wgt[lane * GT + warp] = wv;
+    if (lane == 0) { m_s[warp] = Mx; l_s[warp] = L; }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int s = 0; s < NSL; ++s) {
+    const int sl = tid + s * DEC_THREADS;
+    const int h = sl / (D_HEAD / 2), e2 = sl % (D_HEAD / 2);
+    float a0 = 0.f, a1 = 0.f;
+    if (h < G) {
+#pragma unroll 4
+      for (int w = 0; w < nact; ++w) {
+        const float* src = wp + (w * GT + h) * PS;
+        const float sc = wgt[w * GT + h];
+        a0 = fmaf(src[2 + 2 * e2], sc, a0);
+        a1 = fmaf(src[3 + 2 * e2], sc, a1);
+      }
+    }
+    st.acc[s][0] = a0;
+    st.acc[s][1] = a1;
+  }
+  __syncthreads();
+}
+
+}  // namespace hata

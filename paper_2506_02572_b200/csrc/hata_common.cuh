@@ -105,6 +105,32 @@ __device__ __forceinline__ void full_add(uint32_t a, uint32_t b, uint32_t c, uin
   asm("lop3.b32 %0, %1, %2, %3, 0xE8;" : "=r"(cy) : "r"(a), "r"(b), "r"(c));
 }
 
+// ---------------------------------------------------------------- warp-level tensor core (HMMA)
+// D += A(16x16, row) * B(16x8, col), bf16 inputs, fp32 accumulate.
+// Fragment ownership (gid = lane / 4, tig = lane % 4):
+//   a0: A[gid][2tig..2tig+1]   a1: A[gid+8][2tig..]   a2: A[gid][8+2tig..]   a3: A[gid+8][8+2tig..]
+//   b0: B[2tig..2tig+1][gid]   b1: B[8+2tig..][gid]
+//   d0,d1: D[gid][2tig, 2tig+1]   d2,d3: D[gid+8][2tig, 2tig+1]
+__device__ __forceinline__ void mma_bf16_16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+// Two 8x8 b16 tiles, transposed: lanes 0-7 give the row addresses of tile 0,
+// lanes 8-15 those of tile 1 (16-byte rows).  Yields a B fragment (b0, b1)
+// from a row-major [k][n] smem matrix.
+__device__ __forceinline__ void ldsm_x2_trans(uint32_t& r0, uint32_t& r1, const void* row) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x2.trans.shared.b16 {%0,%1}, [%2];"
+               : "=r"(r0), "=r"(r1)
+               : "r"(smem_u32(row)));
+}
+__device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
+  const __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<const uint32_t*>(&h);
+}
+
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

@@ -75,7 +75,7 @@ DecodePlan plan_decode(int B, int Hq, int Hkv, int d, int rbits, int64_t n_max, 
     if (v >= 1 && v <= DEC_MAX_RANKS && v * units <= sms) M = v;
   }
   const int rowb = d * eb + DEC_ROW_PAD;
-  const int wbytes = (d * rbits * eb + 127) & ~127;
+  const int wbytes = (d * dec_wrow_stride(rbits, eb) + 127) & ~127;
   for (;;) {
     pl.M = M;
     const int64_t per = (n_max + M - 1) / M;
@@ -95,7 +95,7 @@ DecodePlan plan_decode(int B, int Hq, int Hkv, int d, int rbits, int64_t n_max, 
     for (;; --pl.stages) {
       sp.stages = pl.stages;
       pl.smem = decode_smem_layout(sp, GT, eb).total;
-      if (pl.smem <= SMEM_LIMIT || pl.stages == 4) break;
+      if (pl.smem <= SMEM_LIMIT || pl.stages == 2) break;
     }
     pl.d_smem = pl.smem <= SMEM_LIMIT;
     if (!pl.d_smem) {
@@ -135,6 +135,7 @@ cudaError_t launch_decode(DecodeParams& p, const DecodePlan& pl, void* ws, int i
   if (!kern) return cudaErrorNotSupported;
   uint8_t* w = reinterpret_cast<uint8_t*>(ws);
   p.trace = decode_trace_buf();
+  { const char* e = std::getenv("HATA_DEBUG"); p.dbg = e ? std::atoi(e) : 0; }
   p.M = pl.M; p.stages = pl.stages; p.chunk = pl.chunk; p.nbins = pl.nbins; p.rows_cap = pl.rows_cap; p.R_cap = pl.R_cap;
   p.d_smem = pl.d_smem;
   p.ws_sync = pl.M > 1 ? reinterpret_cast<unsigned*>(w + pl.ws_sync) : nullptr;
@@ -152,7 +153,7 @@ cudaError_t launch_decode(DecodeParams& p, const DecodePlan& pl, void* ws, int i
   cfg.stream = s;
   // ranks of a unit meet at a spin barrier: they must be co-resident
   at[0].id = cudaLaunchAttributeCooperative;
-  at[0].val.cooperative = pl.M > 1 ? 1 : 0;
+  at[0].val.cooperative = (pl.M > 1 && !(p.dbg & 8)) ? 1 : 0;
   cfg.attrs = at;
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, kern, (const DecodeParams)p);
@@ -199,4 +200,10 @@ cudaError_t set_decode_trace(void* buf) {
   return cudaSuccess;
 }
 unsigned long long* decode_trace_buf() { return g_trace_buf; }
+
+static __global__ void timestamp_kernel(unsigned long long* dst) { *dst = globaltimer_ns(); }
+cudaError_t launch_timestamp(void* dst, cudaStream_t s) {
+  timestamp_kernel<<<1, 1, 0, s>>>(reinterpret_cast<unsigned long long*>(dst));
+  return cudaGetLastError();
+}
 }  // namespace hata

@@ -22,8 +22,8 @@ namespace hata {
 
 constexpr int DEC_THREADS = 512;
 constexpr int DEC_WARPS = DEC_THREADS / 32;
-constexpr int DEC_STAGE_BYTES = 16384;       // one bulk copy of codes
-constexpr int DEC_MAX_STAGES = 8;            // code ring depth (up to 128 KB in flight)
+constexpr int DEC_STAGE_BYTES = 32768;       // one bulk copy of codes (few large TMA requests)
+constexpr int DEC_MAX_STAGES = 4;            // code ring depth (up to 128 KB in flight)
 constexpr int DEC_D_SMEM_MAX = 16384;        // tokens/CTA whose D (u16) stays in smem
 constexpr int DEC_CHUNK_ALIGN = 64;          // tokens
 constexpr int DEC_MAX_RANKS = 32;            // M cap (histogram exchange is M x nbins per rank)
@@ -71,6 +71,7 @@ struct DecodeParams {
   const void* k_new;       // [B, Hkv, d]
   const void* v_new;
   unsigned long long* trace;   // diagnostics (hata_debug_trace), null = off
+  int dbg;                     // diagnostics: HATA_DEBUG bits (0 in production)
 };
 
 struct DecodeSmem {
@@ -83,6 +84,9 @@ struct DecodeSmem {
 
 __host__ __device__ inline int dec_qstride(int d) { return d + DEC_QS_PAD; }
 __host__ __device__ inline int dec_hist_stride(int nbins) { return (nbins + 3) & ~3; }
+// bytes of one W_g row in smem: padded by 16 so that 8 consecutive rows of a
+// ldmatrix tile fall in distinct banks
+__host__ __device__ inline int dec_wrow_stride(int rbits, int eb) { return rbits * eb + 16; }
 // floats per rank partial block [GT][d+2], padded to 16 bytes
 __host__ __device__ inline int dec_part_stride(int GT, int d) { return (GT * (d + 2) + 3) & ~3; }
 
@@ -95,11 +99,12 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
 }
-#define HATA_TRACE(i)                                                                               \
-  do {                                                                                              \
-    if (p.trace != nullptr && threadIdx.x == 0)                                                     \
-      p.trace[((size_t)blockIdx.y * gridDim.x + blockIdx.x) * 16 + (i)] = globaltimer_ns();         \
-  } while (0)
+constexpr int HATA_TRACE_SLOTS = 32;
+__device__ __forceinline__ void trace_at(unsigned long long* tr, int i) {
+  if (tr != nullptr && threadIdx.x == 0)
+    tr[((size_t)blockIdx.y * gridDim.x + blockIdx.x) * HATA_TRACE_SLOTS + i] = globaltimer_ns();
+}
+#define HATA_TRACE(i) trace_at(p.trace, (i))
 
 // Shared-memory carve-up; identical on host and device.
 __host__ __device__ inline DecodeSmem decode_smem_layout(const DecodeParams& p, int GT, int eb) {
@@ -107,8 +112,8 @@ __host__ __device__ inline DecodeSmem decode_smem_layout(const DecodeParams& p, 
   DecodeSmem s;
   int off = 0;
   s.ring = off; off += p.stages * DEC_STAGE_BYTES;
-  s.W = off; off += up(p.d * p.rbits * eb);
-  s.bars = off; off += up((DEC_MAX_STAGES + 3) * 8);
+  s.W = off; off += up(p.d * dec_wrow_stride(p.rbits, eb));
+  s.bars = off; off += up((DEC_MAX_STAGES + 4) * 8);
   s.hist = off; off += up(p.nbins * 4);
   s.D = off; off += p.d_smem ? up(p.chunk * 2) : 0;
   s.qf = off; off += up((GT + 1) * dec_qstride(p.d) * 4);

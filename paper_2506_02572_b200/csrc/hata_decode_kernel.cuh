@@ -12,6 +12,7 @@
 //   4  gather-fused softmax attention over that share Alg. 3 lines 14-17
 //   5  rank-ordered flash-decoding merge by the last rank to finish
 #pragma once
+#include "hata_attn_mma.cuh"
 #include "hata_decode.cuh"
 
 namespace hata {
@@ -163,6 +164,8 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
   constexpr int EB = sizeof(T);
   constexpr int NSL = AttnState<GT, D_HEAD>::NSL;
   extern __shared__ __align__(1024) uint8_t smem[];
+  HATA_TRACE(31);
+  if (p.dbg & 4) return;                                           // diagnostics: launch cost only
 
   const int M = p.M;
   const int NST = p.stages;
@@ -200,12 +203,8 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
   const bool append = p.k_new != nullptr;
   T* qraw = reinterpret_cast<T*>(smem + L.qraw);                    // [G (+1 key)][d] as stored
 
-  // ---- phase 0: start every stream: W_g, q (+ the new key), then the codes
-  if (tid == 0) {
-    for (int s = 0; s < NST + 3; ++s) mbar_init(&bars[s], 1);
-    fence_mbar_init();
-  }
-  __syncthreads();
+  // ---- phase 0: start every stream: the code chunk by a few large bulk copies
+  // (TMA), W_g / q / the new key by coalesced 16-byte loads of all threads
   auto issue_stage = [&](int s) {
     const int slot = s % NST;
     const int ntok = min(STAGE_TOK, Lcopy - s * STAGE_TOK);
@@ -213,17 +212,50 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
     mbar_arrive_expect_tx(&bars[slot], bytes);
     if (bytes) bulk_g2s(ring + slot * DEC_STAGE_BYTES, cbase + (t0 + (int64_t)s * STAGE_TOK) * W, bytes, &bars[slot]);
   };
-  if (tid == 0) {
-    const uint32_t wbytes = (uint32_t)(p.d * p.rbits * EB);
-    const uint32_t qbytes = (uint32_t)(G * D_HEAD * EB), kbytes = append ? (uint32_t)(D_HEAD * EB) : 0u;
-    mbar_arrive_expect_tx(&bars[NST], wbytes + qbytes + kbytes);
-    bulk_g2s(qraw, qg, qbytes, &bars[NST]);
-    if (append) bulk_g2s(qraw + G * D_HEAD, reinterpret_cast<const T*>(p.k_new) + (int64_t)u * D_HEAD, kbytes, &bars[NST]);
-    bulk_g2s(Ws, reinterpret_cast<const T*>(p.Wh) + (int64_t)g * p.d * p.rbits, wbytes, &bars[NST]);
-    for (int s = 0; s < NST && s < nstages; ++s) issue_stage(s);
+  const int64_t n = p.n[b];                                         // requested before the streams
+  const int wrow = p.rbits * EB;                                    // bytes of one W row
+  const int WROWB = dec_wrow_stride(p.rbits, EB);                   // padded smem row (bank spread)
+  {
+    constexpr int MAXC = 8;                                          // 16-byte chunks per thread (<= 64 KB)
+    const uint4* wsrc = reinterpret_cast<const uint4*>(reinterpret_cast<const T*>(p.Wh) + (int64_t)g * p.d * p.rbits);
+    const int cpr = wrow / 16, nwc = D_HEAD * cpr;                 // chunks per row / in W_g
+    uint4 v[MAXC];
+    // W_g beyond MAXC chunks per thread (fp32 with rbits = 256): earlier batches
+    for (int base = 0; base + MAXC * DEC_THREADS < nwc; base += MAXC * DEC_THREADS) {
+#pragma unroll
+      for (int c = 0; c < MAXC; ++c) v[c] = __ldg(wsrc + base + tid + c * DEC_THREADS);
+#pragma unroll
+      for (int c = 0; c < MAXC; ++c) {
+        const int i = base + tid + c * DEC_THREADS;
+        *reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(Ws) + (i / cpr) * WROWB + (i % cpr) * 16) = v[c];
+      }
+    }
+    const int wlast = (nwc - 1) / (MAXC * DEC_THREADS) * (MAXC * DEC_THREADS);   // last batch
+#pragma unroll
+    for (int c = 0; c < MAXC; ++c)
+      if (wlast + tid + c * DEC_THREADS < nwc) v[c] = __ldg(wsrc + wlast + tid + c * DEC_THREADS);
+    const int nq = G * D_HEAD * EB / 16, nk = append ? D_HEAD * EB / 16 : 0;
+    uint4 vq = make_uint4(0, 0, 0, 0);
+    const uint4* qsrc = reinterpret_cast<const uint4*>(qg);
+    const uint4* ksrc = reinterpret_cast<const uint4*>(reinterpret_cast<const T*>(p.k_new) + (int64_t)u * D_HEAD);
+    if (tid < nq) vq = __ldg(qsrc + tid);
+    else if (tid < nq + nk) vq = __ldg(ksrc + (tid - nq));
+    // the small loads above are in flight ahead of the 128 KB code stream
+    if (tid == 0) {
+      // [0, NST) code ring, NST: unused, NST+1: exchange + D staging, NST+2: partials,
+      // NST+3: attention gather batches
+      for (int s = 0; s < NST + 4; ++s) mbar_init(&bars[s], 1);
+      fence_mbar_init();
+      for (int s = 0; s < NST && s < nstages; ++s) issue_stage(s);
+    }
+#pragma unroll
+    for (int c = 0; c < MAXC; ++c) {
+      const int i = wlast + tid + c * DEC_THREADS;
+      if (i < nwc) *reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(Ws) + (i / cpr) * WROWB + (i % cpr) * 16) = v[c];
+    }
+    if (tid < nq + nk) reinterpret_cast<uint4*>(qraw)[tid] = vq;
   }
   for (int i = tid; i < p.nbins; i += DEC_THREADS) hist[i] = 0;
-  const int64_t n = p.n[b];                                         // latency hidden behind the streams
   const int kp = (int)(n < (int64_t)p.k ? n : (int64_t)p.k);      // k' = min(k, n)  (R10)
   auto chunk_len = [&](int rr) -> int {                            // valid tokens of rank rr
     const int64_t a = (int64_t)rr * per, z = min((int64_t)n, a + per);
@@ -239,7 +271,7 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
   const int64_t pos = n - 1;
   const bool owner = append && n >= 1 && pos >= t0 && pos < t0 + Lr;
   const int NV = G + (owner ? 1 : 0);                                // projected vectors
-  mbar_wait(&bars[NST], 0);
+  __syncthreads();                                                  // W_g, q, k_new in smem
   HATA_TRACE(9);
   for (int i = tid; i < NV * D_HEAD; i += DEC_THREADS) qf[(i / D_HEAD) * QS + i % D_HEAD] = Elem<T>::to_f(qraw[i]);
   if (owner) {
@@ -253,13 +285,54 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
   }
   __syncthreads();
   HATA_TRACE(8);
-  {
-    // projection p[h][bit] = sum_j x_h[j] W[j][bit]: thread = (bit, j-slice), all
-    // vectors at once; slices summed in fixed order (fp32 accumulation, R13)
+  if constexpr (EB == 2) {
+    // bf16: the projection X[NV x d] . W_g[d x rbits] on the tensor cores
+    // (mma.sync m16n8k16, exact bf16 products, fp32 accumulation; R13).
+    // Warp = one 8-bit column tile of the code; Sign + BitPack (Alg. 2 lines
+    // 5-7) straight from the accumulator fragment via ballots.
+    const int gid = lane >> 2, tig = lane & 3;
+    uint8_t* qbytes = reinterpret_cast<uint8_t*>(qw);               // [GT+1][W*4] code bytes
+    for (int nt = warp; nt < p.rbits / 8; nt += DEC_WARPS) {
+      float c[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int k0 = 0; k0 < D_HEAD; k0 += 16) {
+        uint32_t a[4];
+        const float* x0 = qf + gid * QS + k0 + 2 * tig;
+        const float* x1 = qf + (gid + 8) * QS + k0 + 2 * tig;
+        const float2 z = make_float2(0.f, 0.f);
+        const float2 f0 = gid < NV ? *reinterpret_cast<const float2*>(x0) : z;
+        const float2 f1 = gid + 8 < NV ? *reinterpret_cast<const float2*>(x1) : z;
+        const float2 f2 = gid < NV ? *reinterpret_cast<const float2*>(x0 + 8) : z;
+        const float2 f3 = gid + 8 < NV ? *reinterpret_cast<const float2*>(x1 + 8) : z;
+        a[0] = pack_bf16x2(f0.x, f0.y);                             // exact: q, k are bf16
+        a[1] = pack_bf16x2(f1.x, f1.y);
+        a[2] = pack_bf16x2(f2.x, f2.y);
+        a[3] = pack_bf16x2(f3.x, f3.y);
+        uint32_t b0, b1;
+        ldsm_x2_trans(b0, b1, reinterpret_cast<const uint8_t*>(Ws) + (k0 + (lane & 15)) * WROWB + nt * 16);
+        mma_bf16_16816(c, a, b0, b1);
+      }
+      const uint32_t m0 = __ballot_sync(0xffffffffu, c[0] >= 0.f), m1 = __ballot_sync(0xffffffffu, c[1] >= 0.f);
+      const uint32_t m2 = __ballot_sync(0xffffffffu, c[2] >= 0.f), m3 = __ballot_sync(0xffffffffu, c[3] >= 0.f);
+      if (tig == 0) {
+        uint32_t lo = 0, hi = 0;                                    // bits nt*8 .. nt*8+7, LSB-first (R7)
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          lo |= ((m0 >> (gid * 4 + t)) & 1u) << (2 * t) | ((m1 >> (gid * 4 + t)) & 1u) << (2 * t + 1);
+          hi |= ((m2 >> (gid * 4 + t)) & 1u) << (2 * t) | ((m3 >> (gid * 4 + t)) & 1u) << (2 * t + 1);
+        }
+        if (gid < NV) qbytes[gid * W * 4 + nt] = (uint8_t)lo;
+        if (gid + 8 < NV) qbytes[(gid + 8) * W * 4 + nt] = (uint8_t)hi;
+      }
+    }
+  } else {
+    // fp32: thread = (bit, j-slice), all vectors at once (fp32 FMA; slices
+    // summed in fixed order), then Sign + BitPack by ballots
     float* qpart = reinterpret_cast<float*>(smem + L.qp);           // [nparts][GT+1][rbits]
     const int nparts = DEC_THREADS / p.rbits;
     const int bit = tid % p.rbits, part = tid / p.rbits;           // part is warp-uniform
     const int jlen = D_HEAD / nparts;
+    const int wstride = WROWB / EB;
     float acc[GT + 1];
 #pragma unroll
     for (int h = 0; h <= GT; ++h) acc[h] = 0.f;
@@ -267,7 +340,7 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
     for (int j0 = part * jlen; j0 < (part + 1) * jlen; j0 += 4) {
       float wv[4];
 #pragma unroll
-      for (int e = 0; e < 4; ++e) wv[e] = Elem<T>::to_f(wc[(j0 + e) * p.rbits]);
+      for (int e = 0; e < 4; ++e) wv[e] = Elem<T>::to_f(wc[(j0 + e) * wstride]);
 #pragma unroll
       for (int h = 0; h <= GT; ++h) {
         if (h < NV) {
@@ -283,21 +356,22 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
     for (int h = 0; h <= GT; ++h)
       if (h < NV) qpart[(part * (GT + 1) + h) * p.rbits + bit] = acc[h];
     __syncthreads();
-    // Sign + BitPack (Alg. 2 lines 5-7): a warp covers 32 consecutive bits of one vector
     for (int o = tid; o < NV * p.rbits; o += DEC_THREADS) {
       const int h = o / p.rbits, bb = o % p.rbits;
       float sum = 0.f;
       for (int pp = 0; pp < nparts; ++pp) sum += qpart[(pp * (GT + 1) + h) * p.rbits + bb];
       const uint32_t word = __ballot_sync(0xffffffffu, sum >= 0.f);
-      if (lane == 0) {
-        qw[h * W + bb / 32] = word;                                    // row G = new key code
-        if (h < G && p.out_qcodes && r == 0) p.out_qcodes[((int64_t)b * p.Hq + g * G + h) * W + bb / 32] = word;
-        if (h == G)                                                    // Alg. 3 line 9
-          const_cast<uint32_t*>(p.codes)[(int64_t)b * p.c_sb + (int64_t)g * p.c_sh + pos * W + bb / 32] = word;
-      }
+      if (lane == 0) qw[h * W + bb / 32] = word;
     }
   }
   __syncthreads();
+  // publish the query codes (optional output) and the new key's code (Alg. 3 line 9)
+  for (int i = tid; i < NV * W; i += DEC_THREADS) {
+    const int h = i / W, w = i % W;
+    const uint32_t word = qw[i];
+    if (h < G && p.out_qcodes && r == 0) p.out_qcodes[((int64_t)b * p.Hq + g * G + h) * W + w] = word;
+    if (h == G) const_cast<uint32_t*>(p.codes)[(int64_t)b * p.c_sb + (int64_t)g * p.c_sh + pos * W + w] = word;
+  }
   // bit planes of c_b = #{h: q_h bit b set} and of G - c_b (hata_score.cuh)
   if (warp < W) {
     int c = 0;
@@ -320,55 +394,66 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
   HATA_TRACE(1);
   // ---- phase 2: Hamming score + GQA sum (Alg. 3 lines 10-11) + histogram
   const bool mirror = (M > 1) && p.d_smem;          // D also needed by the other ranks
+  auto smem_code = [&](const uint32_t* st, int j, uint32_t (&kc)[W]) {
+    if constexpr (W == 4) {
+      const uint4 v = reinterpret_cast<const uint4*>(st)[j];
+      kc[0] = v.x; kc[1] = v.y; kc[2] = v.z; kc[3] = v.w;
+    } else if constexpr (W == 8) {
+      const uint4 v0 = reinterpret_cast<const uint4*>(st)[2 * j], v1 = reinterpret_cast<const uint4*>(st)[2 * j + 1];
+      kc[0] = v0.x; kc[1] = v0.y; kc[2] = v0.z; kc[3] = v0.w; kc[4] = v1.x; kc[5] = v1.y; kc[6] = v1.z; kc[7] = v1.w;
+    } else {
+#pragma unroll
+      for (int w = 0; w < W; ++w) kc[w] = st[j * W + w];
+    }
+  };
+  int slot = 0;
+  uint32_t parity = 0;
   for (int s = 0; s < nstages; ++s) {
-    const int slot = s % NST;
-    mbar_wait(&bars[slot], (s / NST) & 1);
+    mbar_wait(&bars[slot], parity);
     if (s == 0) HATA_TRACE(10);
     if (s == nstages - 1) HATA_TRACE(13);
-    const int ntok = min(STAGE_TOK, Lr - s * STAGE_TOK);            // valid tokens (< n)
-    const int copied = (int)(((uint32_t)(min(STAGE_TOK, Lcopy - s * STAGE_TOK) * W * 4) & ~15u) / (W * 4));
-    const uint32_t* st = reinterpret_cast<const uint32_t*>(ring + slot * DEC_STAGE_BYTES);
     const int base = s * STAGE_TOK;
+    const int nval = min(STAGE_TOK, Lr - base);                     // valid tokens (< n), may be <= 0
+    const int copied = (int)(((uint32_t)(min(STAGE_TOK, Lcopy - base) * W * 4) & ~15u) / (W * 4));
+    const int npairs = max(0, min(nval, copied)) / 2;
+    const uint32_t* st = reinterpret_cast<const uint32_t*>(ring + slot * DEC_STAGE_BYTES);
+    uint32_t* dst = reinterpret_cast<uint32_t*>(Dloc + base);
+    uint32_t* dst2 = mirror ? reinterpret_cast<uint32_t*>(Dglob + base) : nullptr;
     // two tokens per thread per iteration -> one 32-bit store of a u16 pair
-    for (int j2 = tid; 2 * j2 < ntok; j2 += DEC_THREADS) {
-      uint32_t Dpair[2];
+    for (int j2 = tid; j2 < npairs; j2 += DEC_THREADS) {
+      uint32_t k0[W], k1[W];
+      smem_code(st, 2 * j2, k0);
+      smem_code(st, 2 * j2 + 1, k1);
+      const uint32_t d0 = group_distance<W, J>(k0, A, Bp);
+      const uint32_t d1 = group_distance<W, J>(k1, A, Bp);
+      atomicAdd(&hist[d0], 1u);
+      atomicAdd(&hist[d1], 1u);
+      const uint32_t packed = d0 | (d1 << 16);
+      dst[j2] = packed;
+      if (mirror) dst2[j2] = packed;
+    }
+    // leftovers: an odd last token, or tokens past the 16-byte-rounded copy
+    const int rest = nval - 2 * npairs;
+    if (tid < rest) {
+      const int j = 2 * npairs + tid;
+      uint32_t kc[W];
+      if (j < copied) {
+        smem_code(st, j, kc);
+      } else {
+        const uint32_t* gp = cbase + (t0 + base + j) * W;
 #pragma unroll
-      for (int x = 0; x < 2; ++x) {
-        const int j = 2 * j2 + x;
-        uint32_t kc[W];
-#pragma unroll
-        for (int w = 0; w < W; ++w) kc[w] = 0;
-        if (j < copied) {
-          if constexpr (W == 4) {
-            const uint4 v = reinterpret_cast<const uint4*>(st)[j];
-            kc[0] = v.x; kc[1] = v.y; kc[2] = v.z; kc[3] = v.w;
-          } else if constexpr (W == 8) {
-            const uint4 v0 = reinterpret_cast<const uint4*>(st)[2 * j], v1 = reinterpret_cast<const uint4*>(st)[2 * j + 1];
-            kc[0] = v0.x; kc[1] = v0.y; kc[2] = v0.z; kc[3] = v0.w; kc[4] = v1.x; kc[5] = v1.y; kc[6] = v1.z; kc[7] = v1.w;
-          } else {
-#pragma unroll
-            for (int w = 0; w < W; ++w) kc[w] = st[j * W + w];
-          }
-        } else if (j < ntok) {
-          const uint32_t* gp = cbase + (t0 + base + j) * W;
-#pragma unroll
-          for (int w = 0; w < W; ++w) kc[w] = __ldg(gp + w);
-        }
-        if (j < ntok) {
-          Dpair[x] = group_distance<W, J>(kc, A, Bp);
-          atomicAdd(&hist[Dpair[x]], 1u);
-        } else {
-          Dpair[x] = 0xffffu;
-        }
+        for (int w = 0; w < W; ++w) kc[w] = __ldg(gp + w);
       }
-      const uint32_t packed = Dpair[0] | (Dpair[1] << 16);
-      reinterpret_cast<uint32_t*>(Dloc + base)[j2] = packed;
-      if (mirror) reinterpret_cast<uint32_t*>(Dglob + base)[j2] = packed;
+      const uint32_t dv = group_distance<W, J>(kc, A, Bp);
+      atomicAdd(&hist[dv], 1u);
+      Dloc[base + j] = (uint16_t)dv;
+      if (mirror) Dglob[base + j] = (uint16_t)dv;
     }
     if (recycle) {                                                  // refill the slot just consumed
       __syncthreads();
       if (tid == 0 && s + NST < nstages) issue_stage(s + NST);
     }
+    if (++slot == NST) { slot = 0; parity ^= 1u; }
   }
   __syncthreads();                                                  // every D / histogram update done
   if (owner && tid == 0) {
@@ -401,6 +486,46 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
     if (tid == 0) {
       __threadfence();
       atomicAdd(sync, 1u);
+    }
+    // While the other ranks finish scoring: warm L2 with the K/V rows this
+    // rank will most likely select (its own tokens below a local estimate of
+    // the threshold), so the gather after the selection hits L2.  A pure
+    // prefetch: the selection itself is decided exactly after the exchange.
+    if (!p.cand_mode && !(p.dbg & 2)) {
+      const int want = (int)(((int64_t)kp * Lr + n - 1) / (n > 0 ? n : 1)) * 9 / 8 + 4;
+      int mysum = 0, tb[5];
+      const int BPT = (p.nbins + DEC_THREADS - 1) / DEC_THREADS, i0 = tid * BPT;
+#pragma unroll
+      for (int q = 0; q < 5; ++q) {
+        tb[q] = (q < BPT && i0 + q < p.nbins) ? (int)hist[i0 + q] : 0;
+        mysum += tb[q];
+      }
+      int total;
+      int cum = block_excl_scan(mysum, misc + 16, total);
+      if (tid == 0) misc[4] = p.nbins;
+      __syncthreads();
+#pragma unroll
+      for (int q = 0; q < 5; ++q) {
+        if (cum < want && cum + tb[q] >= want) misc[4] = i0 + q;
+        cum += tb[q];
+      }
+      __syncthreads();
+      const int test = misc[4];                                     // prefetch tokens with D <= test
+      const __nv_bfloat16* Kb = reinterpret_cast<const __nv_bfloat16*>(p.K) + (int64_t)b * p.kv_sb + (int64_t)g * p.kv_sh;
+      const __nv_bfloat16* Vb = reinterpret_cast<const __nv_bfloat16*>(p.V) + (int64_t)b * p.kv_sb + (int64_t)g * p.kv_sh;
+      for (int j = tid * 8; j < Lr; j += DEC_THREADS * 8) {
+        uint32_t ltm, tim;
+        d_masks(Dloc, !p.d_smem, j, Lr, test + 1, ltm, tim);
+        while (ltm) {
+          const int e = __ffs(ltm) - 1;
+          ltm &= ltm - 1;
+          const int64_t t = t0 + j + e;
+          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(Kb + t * p.kv_st), "r"(D_HEAD * EB) : "memory");
+          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(Vb + t * p.kv_st), "r"(D_HEAD * EB) : "memory");
+        }
+      }
+    }
+    if (tid == 0) {
       while (ld_acquire_gpu(sync) < (unsigned)M) {
       }
       // other ranks' generic-proxy writes -> this thread's async-proxy (bulk copy) reads
@@ -560,9 +685,14 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
   if (!p.cand_mode) {
     const T* Kb = reinterpret_cast<const T*>(p.K) + (int64_t)b * p.kv_sb + (int64_t)g * p.kv_sh;
     const T* Vb = reinterpret_cast<const T*>(p.V) + (int64_t)b * p.kv_sb + (int64_t)g * p.kv_sh;
-    float* sc = reinterpret_cast<float*>(smem + L.sc);
-    attend_rows<T, GT, D_HEAD>(rows, P1 - P0, Kb, Vb, p.kv_st, qf, G, p.scale, smem + L.kv, sc, p.rows_cap, L.rb,
-                               m_s, l_s, corr_s, st);
+    if constexpr (EB == 2) {
+      attend_rows_mma<GT, D_HEAD>(rows, P1 - P0, Kb, Vb, p.kv_st, qf, G, p.scale, smem + L.kv, p.rows_cap, L.rb,
+                                  m_s, l_s, st, &bars[NST + 3], p.trace);
+    } else {
+      float* sc = reinterpret_cast<float*>(smem + L.sc);
+      attend_rows<T, GT, D_HEAD>(rows, P1 - P0, Kb, Vb, p.kv_st, qf, G, p.scale, smem + L.kv, sc, p.rows_cap, L.rb,
+                                 m_s, l_s, corr_s, st);
+    }
   }
   HATA_TRACE(6);
 
@@ -617,12 +747,15 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
     float* wgt = reinterpret_cast<float*>(smem + L.hm + ((M * PB * 4 + 127) & ~127));   // [M][GT] weights
     if (tid == 0) {
       __threadfence();
+      HATA_TRACE(24);
       asm volatile("fence.proxy.async.global;" ::: "memory");
       const uint32_t bytes = (uint32_t)(M * PB * 4);
       mbar_arrive_expect_tx(&bars[NST + 2], bytes);
       bulk_g2s(sp, p.ws_part + (int64_t)u * M * PB, bytes, &bars[NST + 2]);
+      HATA_TRACE(25);
     }
     mbar_wait(&bars[NST + 2], 0);
+    HATA_TRACE(26);
     // per-head max, then per-(rank, head) weights e^{m_r - M_h}, then L_h
     if (tid < G) {
       float Mx = -INFINITY;

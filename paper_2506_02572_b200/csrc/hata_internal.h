@@ -72,3 +72,6 @@ cudaError_t set_decode_trace(void* buf);
 namespace hata {
 unsigned long long* decode_trace_buf();
 }  // namespace hata
+namespace hata {
+cudaError_t launch_timestamp(void* dst, cudaStream_t s);
+}  // namespace hata
