@@ -22,10 +22,11 @@
  *      code cache codes  [B, H_kv, cap, rbits/32] uint32 word strides
  *                        {sb, sh, st}; st must equal rbits/32 (rows packed),
  *                        rows 16-byte aligned when rbits >= 128.
- *      hash weight W     [H_kv, d, rbits] contiguous, same dtype as K
- *                        (one W_H per KV head, shared by its G query heads; R4).
- *      queries    q      [B, H_q, d] contiguous; query head h reads KV head
- *                        h / G with G = H_q / H_kv (R5).
+ *      hash weight W     [H_kv, d, rbits] contiguous, same dtype as K,
+ *                        16-byte aligned (one W_H per KV head, shared by its
+ *                        G query heads; R4).
+ *      queries    q      [B, H_q, d] contiguous, 16-byte aligned; query head h
+ *                        reads KV head h / G with G = H_q / H_kv (R5).
  *  - Codes: bit b of a row is 1 iff (x . W[:, b]) >= 0 (sign(0) -> +1, R6),
  *    stored LSB-first in word b / 32 (R7).  Projections accumulate in fp32.
  *  - Supported: d == 128; rbits in {32, 64, 128, 256}; G = H_q/H_kv <= 8;
@@ -214,10 +215,10 @@ const char* hata_last_error(void);
 const char* hata_version(void);
 
 /* Diagnostics only.  buf: NULL (off, the default) or device memory of at least
- * 16 * (number of decode CTAs) uint64; while set, every decode launch writes
- * %globaltimer stamps (ns) of its phase boundaries to buf[cta * 16 + phase]
- * (0 start, 1 q-hash done, 2 score done, 3 histograms exchanged, 4 D staged,
- * 5 selection done, 6 attention done, 7 end).  Not for production use. */
+ * 64 * (number of decode CTAs) uint64; while set, every decode launch writes
+ * %globaltimer stamps (ns) of its phase boundaries to buf[cta * 64 + i],
+ * i < 32, and clock64 stamps to buf[cta * 64 + 32 + i] (slot meanings:
+ * tools/trace_decode.py).  Not for production use. */
 hata_status hata_debug_trace(void* buf);
 /* Diagnostics only: enqueue a 1-thread kernel that stores %globaltimer (ns)
  * to *dst (device uint64), to bracket a traced launch on the same stream. */

@@ -10,7 +10,8 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libhata.so")
+# HATA_LIB=libhata_trace.so selects the diagnostics build (tools/trace_decode.py)
+LIB_PATH = os.path.join(_HERE, os.environ.get("HATA_LIB", "libhata.so"))
 
 HATA_OK = 0
 HATA_F32 = 0

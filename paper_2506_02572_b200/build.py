@@ -14,12 +14,15 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
 INCLUDE = os.path.join(ROOT, "include")
-OUT = os.path.join(HERE, "libhata.so")
-OBJ = os.path.join(HERE, "_build")
+# HATA_TRACE_BUILD=1: the diagnostics variant (phase stamps compiled in) for
+# tools/trace_decode.py -> libhata_trace.so; the product is libhata.so
+TRACE = os.environ.get("HATA_TRACE_BUILD") == "1"
+OUT = os.path.join(HERE, "libhata_trace.so" if TRACE else "libhata.so")
+OBJ = os.path.join(HERE, "_build_trace" if TRACE else "_build")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
-         "-Xptxas", "-v", "-I", INCLUDE, "-I", CSRC]
+         "-Xptxas", "-v", "-I", INCLUDE, "-I", CSRC] + (["-DHATA_TRACE_ENABLED=1"] if TRACE else [])
 SOURCES = ["hata_abi.cu", "hata_decode.cu", "hata_hash.cu", "hata_hash_tc.cu", "hata_shard.cu"]
 
 

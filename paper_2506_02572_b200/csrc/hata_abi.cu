@@ -166,7 +166,7 @@ static hata_status decode_common(const void* q, const void* K, const void* V, ha
   if (!codes_layout_ok(codes, cs, rbits)) return HATA_ERR_INVALID_ARG;
   if (!cand_mode && (!kv_layout_ok(K, kvs, elem_bytes(dt), d) || !kv_layout_ok(V, kvs, elem_bytes(dt), d)))
     return HATA_ERR_INVALID_ARG;
-  if (!aligned(q, 16)) return HATA_ERR_INVALID_ARG;
+  if (!aligned(q, 16) || !aligned(W, 16)) return HATA_ERR_INVALID_ARG;   // bulk-copied (TMA)
   const hata::DecodePlan pl = get_plan(B, H_q, H_kv, d, rbits, n_max, k, elem_bytes(dt));
   if (pl.GT < 0) return HATA_ERR_UNSUPPORTED;
   if (pl.ws_total && (!workspace || ws_bytes < pl.ws_total || !aligned(workspace, 256))) return HATA_ERR_WORKSPACE;

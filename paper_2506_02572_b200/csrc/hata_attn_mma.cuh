@@ -17,7 +17,7 @@ namespace hata {
 
 template <int GT, int D_HEAD>
 __device__ __forceinline__ void attend_rows_mma(const int32_t* rows, int Rr, const __nv_bfloat16* __restrict__ Kb,
-                                                const __nv_bfloat16* __restrict__ Vb, int64_t kv_st, const float* qf,
+                                                const __nv_bfloat16* __restrict__ Vb, int64_t kv_st, const __nv_bfloat16* qb,
                                                 int G, float scale, uint8_t* kvbuf, int rows_cap, int rowb,
                                                 float* m_s, float* l_s, AttnState<GT, D_HEAD>& st,
                                                 uint64_t* bar, unsigned long long* tr = nullptr, int tb = 16) {
@@ -28,14 +28,18 @@ __device__ __forceinline__ void attend_rows_mma(const int32_t* rows, int Rr, con
   constexpr int NSL = AttnState<GT, D_HEAD>::NSL;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int gid = lane >> 2, tig = lane & 3;
-  const int QS = dec_qstride(D_HEAD);
   uint8_t* Ks = kvbuf;
   uint8_t* Vs = kvbuf + rows_cap * rowb;
 
-  // Q as A fragments (exact: q is bf16), built per k-step from smem; heads
-  // >= G and rows 8..15 are zero
-  const float* qrow = qf + (gid < G ? gid : 0) * QS + 2 * tig;
-  const bool qvalid = gid < G;
+  // Q as A fragments held in registers for the whole call, read once from the
+  // bf16 rows as stored (qb: [G][D_HEAD] smem); heads >= G and rows 8..15 are zero
+  uint32_t qa[KS][2];
+#pragma unroll
+  for (int ks = 0; ks < KS; ++ks) {
+    const uint32_t* x = reinterpret_cast<const uint32_t*>(qb + gid * D_HEAD + ks * 16 + 2 * tig);
+    qa[ks][0] = gid < G ? x[0] : 0u;
+    qa[ks][1] = gid < G ? x[4] : 0u;
+  }
   float O[NT][4];
 #pragma unroll
   for (int t = 0; t < NT; ++t) O[t][0] = O[t][1] = O[t][2] = O[t][3] = 0.f;
@@ -51,7 +55,7 @@ __device__ __forceinline__ void attend_rows_mma(const int32_t* rows, int Rr, con
     constexpr uint32_t ROWBYTES = D_HEAD * 2;
     if (tid == 0) mbar_arrive_expect_tx(bar, 2u * ROWBYTES * (uint32_t)nb);
     __syncthreads();
-    if (r0 == 0) trace_at(tr, tb + 4);
+    if (r0 == 0) HATA_TRACE_AT(tr, tb + 4);
     // request i -> warp i % NW, lane i / NW: a warp issues its bulk copies one
     // lane after another, so spread them over all warps
     for (int i = lane * DEC_WARPS + warp; i < 2 * nb; i += DEC_THREADS) {
@@ -59,10 +63,10 @@ __device__ __forceinline__ void attend_rows_mma(const int32_t* rows, int Rr, con
       const __nv_bfloat16* src = (which ? Vb : Kb) + (int64_t)rows[r0 + rr] * kv_st;
       bulk_g2s((which ? Vs : Ks) + rr * rowb, src, ROWBYTES, bar);
     }
-    if (r0 == 0) trace_at(tr, tb + 3);
+    if (r0 == 0) HATA_TRACE_AT(tr, tb + 3);
     mbar_wait(bar, bpar);
     bpar ^= 1u;
-    if (r0 == 0) trace_at(tr, tb);
+    if (r0 == 0) HATA_TRACE_AT(tr, tb);
     for (int g0 = warp * 16; g0 < nb; g0 += DEC_WARPS * 16) {
       active = true;
       // S = Q K^T for rows g0 .. g0+15 (two 8-row tiles)
@@ -77,9 +81,7 @@ __device__ __forceinline__ void attend_rows_mma(const int32_t* rows, int Rr, con
         for (int ks = 0; ks < KS; ++ks) {
           const uint32_t b0 = *reinterpret_cast<const uint32_t*>(kr + ks * 32);
           const uint32_t b1 = *reinterpret_cast<const uint32_t*>(kr + ks * 32 + 16);
-          const float2 f0 = *reinterpret_cast<const float2*>(qrow + ks * 16);
-          const float2 f2 = *reinterpret_cast<const float2*>(qrow + ks * 16 + 8);
-          const uint32_t a[4] = {qvalid ? pack_bf16x2(f0.x, f0.y) : 0u, 0u, qvalid ? pack_bf16x2(f2.x, f2.y) : 0u, 0u};
+          const uint32_t a[4] = {qa[ks][0], 0u, qa[ks][1], 0u};
           mma_bf16_16816(S[t], a, b0, b1);
         }
       }
@@ -133,17 +135,15 @@ __device__ __forceinline__ void attend_rows_mma(const int32_t* rows, int Rr, con
   }
   // merge the warps in fixed order: smem [warp][GT][D_HEAD + 2] over the K/V area
   __syncthreads();
-  trace_at(tr, tb + 1);
+  HATA_TRACE_AT(tr, tb + 1);
   float* wp = reinterpret_cast<float*>(kvbuf);
   const int PS = D_HEAD + 2;
   if (gid < G) {
     float* dst = wp + (warp * GT + gid) * PS;
     if (tig == 0) { dst[0] = active ? m_run : -INFINITY; dst[1] = active ? l_run : 0.f; }
 #pragma unroll
-    for (int t = 0; t < NT; ++t) {
-      dst[2 + t * 8 + 2 * tig] = O[t][0] + O[t][2];                // hi + lo halves of P
-      dst[2 + t * 8 + 2 * tig + 1] = O[t][1] + O[t][3];
-    }
+    for (int t = 0; t < NT; ++t)                                    // hi + lo halves of P
+      *reinterpret_cast<float2*>(dst + 2 + t * 8 + 2 * tig) = make_float2(O[t][0] + O[t][2], O[t][1] + O[t][3]);
   }
   // only the first nact warps ever held rows
   const int nact = min(DEC_WARPS, (min(Rr, rows_cap) + 15) / 16);
@@ -164,6 +164,7 @@ __device__ __forceinline__ void attend_rows_mma(const int32_t* rows, int Rr, con
     if (lane == 0) { m_s[warp] = Mx; l_s[warp] = L; }
   }
   __syncthreads();
+  HATA_TRACE_AT(tr, 29);
 #pragma unroll
   for (int s = 0; s < NSL; ++s) {
     const int sl = tid + s * DEC_THREADS;
@@ -174,14 +175,16 @@ __device__ __forceinline__ void attend_rows_mma(const int32_t* rows, int Rr, con
       for (int w = 0; w < nact; ++w) {
         const float* src = wp + (w * GT + h) * PS;
         const float sc = wgt[w * GT + h];
-        a0 = fmaf(src[2 + 2 * e2], sc, a0);
-        a1 = fmaf(src[3 + 2 * e2], sc, a1);
+        const float2 v = *reinterpret_cast<const float2*>(src + 2 + 2 * e2);
+        a0 = fmaf(v.x, sc, a0);
+        a1 = fmaf(v.y, sc, a1);
       }
     }
     st.acc[s][0] = a0;
     st.acc[s][1] = a1;
   }
   __syncthreads();
+  HATA_TRACE_AT(tr, 30);
 }
 
 }  // namespace hata

@@ -82,7 +82,7 @@ DecodePlan plan_decode(int B, int Hq, int Hkv, int d, int rbits, int64_t n_max, 
     pl.chunk = (int)((per + DEC_CHUNK_ALIGN - 1) / DEC_CHUNK_ALIGN * DEC_CHUNK_ALIGN);
     if (pl.chunk < DEC_CHUNK_ALIGN) pl.chunk = DEC_CHUNK_ALIGN;
     const int64_t kmax = k < n_max ? k : n_max;
-    pl.R_cap = (int)((kmax + M - 1) / M);
+    pl.R_cap = (int)(kmax < pl.chunk ? kmax : pl.chunk);         // a rank may hold every selected row
     if (pl.R_cap < 1) pl.R_cap = 1;
     pl.rows_global = pl.R_cap > ROWS_SMEM_MAX;
     // shared memory: the code ring holds the whole chunk when it can (8 x 16 KB);
@@ -114,17 +114,16 @@ DecodePlan plan_decode(int B, int Hq, int Hkv, int d, int rbits, int64_t n_max, 
     if (rc > pl.R_cap) rc = pl.R_cap;
     if (rc < 1) rc = 1;
     pl.rows_cap = rc;
-    const bool fits = M * dec_hist_stride(pl.nbins) * 4 + 128 <= region &&
-                      M * (dec_part_stride(GT, d) + GT) * 4 + 256 <= region;
-    if (fits || M == 1) break;
-    --M;
+    break;
   }
+  const int hs = dec_hist_stride(pl.nbins + 1);
   // workspace (every section 256-byte aligned)
   size_t off = 0;
   pl.ws_sync = off;  off += M > 1 ? up256((size_t)units * 2 * 4) : 0;
-  pl.ws_hist = off;  off += M > 1 ? up256((size_t)units * M * dec_hist_stride(pl.nbins) * 4) : 0;
+  pl.ws_hist = off;  off += M > 1 ? up256((size_t)units * M * hs * 4) : 0;
+  pl.ws_tot = off;   off += M > 1 ? up256((size_t)units * hs * 4) : 0;
   pl.ws_part = off;  off += M > 1 ? up256((size_t)units * M * dec_part_stride(GT, d) * 4) : 0;
-  pl.ws_D = off;     off += (M > 1 || !pl.d_smem) ? up256((size_t)units * M * pl.chunk * 2) : 0;
+  pl.ws_D = off;     off += !pl.d_smem ? up256((size_t)units * M * dec_dchunk(pl.chunk) * 2) : 0;
   pl.ws_rows = off;  off += pl.rows_global ? up256((size_t)units * M * pl.R_cap * 4) : 0;
   pl.ws_total = off;
   return pl;
@@ -141,7 +140,8 @@ cudaError_t launch_decode(DecodeParams& p, const DecodePlan& pl, void* ws, int i
   p.ws_sync = pl.M > 1 ? reinterpret_cast<unsigned*>(w + pl.ws_sync) : nullptr;
   p.ws_hist = pl.M > 1 ? reinterpret_cast<int32_t*>(w + pl.ws_hist) : nullptr;
   p.ws_part = pl.M > 1 ? reinterpret_cast<float*>(w + pl.ws_part) : nullptr;
-  p.ws_D = (pl.M > 1 || !pl.d_smem) ? reinterpret_cast<uint16_t*>(w + pl.ws_D) : nullptr;
+  p.ws_tot = pl.M > 1 ? reinterpret_cast<int32_t*>(w + pl.ws_tot) : nullptr;
+  p.ws_D = !pl.d_smem ? reinterpret_cast<uint16_t*>(w + pl.ws_D) : nullptr;
   p.ws_rows = pl.rows_global ? reinterpret_cast<int32_t*>(w + pl.ws_rows) : nullptr;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, pl.smem);
   if (e != cudaSuccess) return e;

@@ -7,10 +7,10 @@
 // the grid (M x units) covers the 148 SMs even when B*H_kv is small.  The
 // launch is cooperative (all CTAs co-resident) and the ranks of a unit meet
 // exactly once, at a global-memory barrier after scoring, to exchange their
-// D-histograms.  Every rank then derives the same threshold, per-rank tie
-// quotas and output offsets, takes an equal share of the k' selected rows
-// (re-scanning the D arrays it needs from L2), attends to them, and the last
-// rank to finish merges the M softmax partials in rank order.
+// D-histogram prefix counts.  Every rank then derives the same threshold,
+// its own tie quota and output offset, compacts its OWN selected tokens in
+// token order, attends to them, and the last rank to finish merges the M
+// softmax partials in rank order.
 //
 // PAPER: Alg. 3 lines 6, 10-17; §4.
 // Readings R1-R20 are listed in DESIGN.md.
@@ -20,7 +20,7 @@
 
 namespace hata {
 
-constexpr int DEC_THREADS = 512;
+constexpr int DEC_THREADS = 256;
 constexpr int DEC_WARPS = DEC_THREADS / 32;
 constexpr int DEC_STAGE_BYTES = 32768;       // one bulk copy of codes (few large TMA requests)
 constexpr int DEC_MAX_STAGES = 4;            // code ring depth (up to 128 KB in flight)
@@ -52,12 +52,13 @@ struct DecodeParams {
   int chunk;               // tokens per rank (capacity), multiple of DEC_CHUNK_ALIGN
   int nbins;               // G*rbits + 1
   int rows_cap;            // rows per attention batch held in smem
-  int R_cap;               // selected rows per rank (capacity of the rows list)
+  int R_cap;               // selected rows per rank (capacity of the rows list) = min(k', chunk)
   int32_t* ws_rows;        // [units, M, R_cap] rows list when it does not fit in smem, else null
-  int d_smem;              // 1: this rank's D lives in smem (mirrored to ws_D when M > 1)
+  int d_smem;              // 1: this rank's D lives in smem, else in ws_D
   // workspace (global); zero-initialised once, left zeroed by every launch
-  int32_t* ws_hist;        // [units, M, nbins]            (M > 1)
-  uint16_t* ws_D;          // [units, M, chunk]            (M > 1 or !d_smem)
+  int32_t* ws_hist;        // [units, M, hs] exclusive prefix counts cum_r[0..nbins]   (M > 1)
+  int32_t* ws_tot;         // [units, hs] sum over the ranks of cum_r (atomics)        (M > 1)
+  uint16_t* ws_D;          // [units, M, chunk] D when it does not fit in smem (!d_smem)
   float* ws_part;          // [units, M, GT, d+2]          (M > 1)
   unsigned* ws_sync;       // [units, 2]: barrier, done    (M > 1)
   // sequence-shard phase 1 (hata_shard_candidates): stop after the select and
@@ -83,6 +84,9 @@ struct DecodeSmem {
 };
 
 __host__ __device__ inline int dec_qstride(int d) { return d + DEC_QS_PAD; }
+// tokens of a rank's D buffer: the chunk rounded up to 8 * DEC_THREADS (the
+// selection reads whole uint4 blocks of 8 tokens per thread)
+__host__ __device__ inline int dec_dchunk(int chunk) { return (chunk + 8 * DEC_THREADS - 1) / (8 * DEC_THREADS) * (8 * DEC_THREADS); }
 __host__ __device__ inline int dec_hist_stride(int nbins) { return (nbins + 3) & ~3; }
 // bytes of one W_g row in smem: padded by 16 so that 8 consecutive rows of a
 // ldmatrix tile fall in distinct banks
@@ -99,12 +103,33 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
 }
-constexpr int HATA_TRACE_SLOTS = 32;
+constexpr int HATA_TRACE_SLOTS = 64;   // [0, 32) %globaltimer stamps, [32, 64) clock64 stamps
 __device__ __forceinline__ void trace_at(unsigned long long* tr, int i) {
   if (tr != nullptr && threadIdx.x == 0)
     tr[((size_t)blockIdx.y * gridDim.x + blockIdx.x) * HATA_TRACE_SLOTS + i] = globaltimer_ns();
 }
+__device__ __forceinline__ void clock_at(unsigned long long* tr, int i) {
+  if (tr != nullptr && threadIdx.x == 0) {
+    unsigned long long c;
+    asm volatile("mov.u64 %0, %%clock64;" : "=l"(c)::"memory");
+    tr[((size_t)blockIdx.y * gridDim.x + blockIdx.x) * HATA_TRACE_SLOTS + 32 + i] = c;
+  }
+}
+// Stamps are compiled in only for the diagnostics build (libhata_trace.so,
+// HATA_TRACE_ENABLED=1); the production kernel carries none of this code.
+#ifndef HATA_TRACE_ENABLED
+#define HATA_TRACE_ENABLED 0
+#endif
+#define HATA_DIAG HATA_TRACE_ENABLED
+#if HATA_TRACE_ENABLED
 #define HATA_TRACE(i) trace_at(p.trace, (i))
+#define HATA_CLK(i) clock_at(p.trace, (i))
+#define HATA_TRACE_AT(tr, i) trace_at((tr), (i))
+#else
+#define HATA_TRACE(i) ((void)0)
+#define HATA_CLK(i) ((void)0)
+#define HATA_TRACE_AT(tr, i) ((void)0)
+#endif
 
 // Shared-memory carve-up; identical on host and device.
 __host__ __device__ inline DecodeSmem decode_smem_layout(const DecodeParams& p, int GT, int eb) {
@@ -115,10 +140,10 @@ __host__ __device__ inline DecodeSmem decode_smem_layout(const DecodeParams& p, 
   s.W = off; off += up(p.d * dec_wrow_stride(p.rbits, eb));
   s.bars = off; off += up((DEC_MAX_STAGES + 4) * 8);
   s.hist = off; off += up(p.nbins * 4);
-  s.D = off; off += p.d_smem ? up(p.chunk * 2) : 0;
+  s.D = off; off += p.d_smem ? up(dec_dchunk(p.chunk) * 2) : 0;
   s.qf = off; off += up((GT + 1) * dec_qstride(p.d) * 4);
   s.qw = off; off += up((GT + 1) * (p.rbits / 32) * 4);
-  s.qraw = off; off += up((GT + 1) * p.d * eb);
+  s.qraw = off; off += up((GT + 2) * p.d * eb);   // q rows, new key, new value
   s.planes = off; off += up(2 * 4 * 8 * 4);
   s.rows = off; off += p.ws_rows ? 0 : up(p.R_cap * 4);
   s.red = off; off += up((DEC_MAX_RANKS * 4 + 64) * 4);
@@ -144,6 +169,19 @@ __device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
   unsigned v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
+}
+// Release-add without a return value (arrival at a barrier counter).
+__device__ __forceinline__ void red_add_release_gpu(unsigned* p, unsigned v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+// Add with acquire-release semantics, returning the old value.
+__device__ __forceinline__ unsigned atom_add_acq_rel_gpu(unsigned* p, unsigned v) {
+  unsigned old;
+  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+__device__ __forceinline__ void prefetch_l2(const void* g, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(g), "r"(bytes) : "memory");
 }
 __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem_dst)), "l"(gsrc) : "memory");

@@ -46,15 +46,38 @@ __device__ __forceinline__ int block_excl_scan(int v, int* buf, int& total) {
   return buf[warp] + inc - v;
 }
 
-// One rank's D array as seen by the selection scan.
-struct ChunkRef {
-  const uint16_t* D;   // 16-byte aligned
-  int L;               // tokens
-  int quota;           // ties (D == thr) selected from this chunk
-  int base;            // selection position of its first selected token
-  int fromg;           // D lives in global memory (L2): load with ld.cg
-  int tok0;            // sequence index of its token 0
-};
+// Two block-wide exclusive scans at once (a and b).  Returns the exclusive
+// prefix of a; eb = that of b; ta, tb = the totals.  buf: >= 2 * (DEC_WARPS + 1) ints.
+__device__ __forceinline__ int block_excl_scan2(int a, int b, int* buf, int& eb, int& ta, int& tb) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int ia = a, ib = b;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int ya = __shfl_up_sync(0xffffffffu, ia, o);
+    const int yb = __shfl_up_sync(0xffffffffu, ib, o);
+    if (lane >= o) { ia += ya; ib += yb; }
+  }
+  __syncthreads();
+  if (lane == 31) { buf[warp] = ia; buf[DEC_WARPS + 1 + warp] = ib; }
+  __syncthreads();
+  if (warp == 0) {
+    const int wa = lane < DEC_WARPS ? buf[lane] : 0, wb = lane < DEC_WARPS ? buf[DEC_WARPS + 1 + lane] : 0;
+    int xa = wa, xb = wb;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int ya = __shfl_up_sync(0xffffffffu, xa, o);
+      const int yb = __shfl_up_sync(0xffffffffu, xb, o);
+      if (lane >= o) { xa += ya; xb += yb; }
+    }
+    if (lane < DEC_WARPS) { buf[lane] = xa - wa; buf[DEC_WARPS + 1 + lane] = xb - wb; }
+    if (lane == DEC_WARPS - 1) { buf[DEC_WARPS] = xa; buf[2 * DEC_WARPS + 1] = xb; }
+  }
+  __syncthreads();
+  ta = buf[DEC_WARPS];
+  tb = buf[2 * DEC_WARPS + 1];
+  eb = buf[DEC_WARPS + 1 + warp] + ib - b;
+  return buf[warp] + ia - a;
+}
 
 // 8-bit masks of (D < thr) and (D == thr) for tokens j .. j+7 of a chunk,
 // tokens >= s1 masked out.
@@ -83,80 +106,6 @@ __device__ __forceinline__ void d_masks(const uint16_t* Dc, bool fromg, int j, i
   }
 }
 
-// Order-preserving compaction over the chunks ch[0..nch) at once: the warps
-// are split evenly between the chunks; a lane owns 8 consecutive tokens, a
-// warp a contiguous segment.  Token t of chunk c is selected iff D < thr, or
-// D == thr and its tie rank within the chunk is < quota; its selection
-// position is base + #selected before it in the chunk.  Positions in
-// [P0, P1) are passed to emit(pos, token, D).  All threads must call.
-template <typename Emit>
-__device__ __forceinline__ void scan_chunks(const ChunkRef* ch, int nch, int thr, int P0, int P1, int* wcnt,
-                                            Emit emit) {
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int c0 = 0; c0 < nch; c0 += DEC_WARPS) {
-    const int n_here = min(DEC_WARPS, nch - c0);
-    const int wpc = DEC_WARPS / n_here;                 // warps per chunk
-    const int ci = warp / wpc, sub = warp % wpc;
-    const bool active = ci < n_here;
-    ChunkRef c = {};
-    if (active) c = ch[c0 + ci];
-    const int seg = ((c.L + wpc - 1) / wpc + 255) & ~255;
-    const int s0 = active ? min(c.L, sub * seg) : 0, s1 = active ? min(c.L, s0 + seg) : 0;
-    int lt_w = 0, ti_w = 0;
-    for (int j0 = s0; j0 < s1; j0 += 256) {
-      uint32_t ltm = 0, tim = 0;
-      if (j0 + 8 * lane < s1) d_masks(c.D, c.fromg, j0 + 8 * lane, s1, thr, ltm, tim);
-      lt_w += __popc(ltm);
-      ti_w += __popc(tim);
-    }
-    lt_w = warp_sum_i(lt_w);
-    ti_w = warp_sum_i(ti_w);
-    __syncthreads();                                   // wcnt reuse guard
-    if (lane == 0) { wcnt[2 * warp] = lt_w; wcnt[2 * warp + 1] = ti_w; }
-    __syncthreads();
-    if (active) {
-      int lt_b = 0, ti_b = 0;
-      for (int w = ci * wpc; w < warp; ++w) { lt_b += wcnt[2 * w]; ti_b += wcnt[2 * w + 1]; }
-      const int q = c.quota, base = c.base;
-      const int seg_first = base + lt_b + min(ti_b, q);
-      const int seg_last = base + lt_b + lt_w + min(ti_b + ti_w, q);   // exclusive
-      if (seg_last > P0 && seg_first < P1) {
-        for (int j0 = s0; j0 < s1; j0 += 256) {
-          const int j = j0 + 8 * lane;
-          uint32_t ltm = 0, tim = 0;
-          if (j < s1) d_masks(c.D, c.fromg, j, s1, thr, ltm, tim);
-          const int mine = __popc(ltm) | (__popc(tim) << 16);
-          int incl = mine;
-#pragma unroll
-          for (int o = 1; o < 32; o <<= 1) {
-            const int y = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += y;
-          }
-          const int excl = incl - mine;
-          const int tot = __shfl_sync(0xffffffffu, incl, 31);
-          const int ltl = lt_b + (excl & 0xffff), til = ti_b + (excl >> 16);
-          uint32_t any = ltm | tim;
-          while (any) {
-            const int e = __ffs(any) - 1;
-            any &= any - 1;
-            const uint32_t below = (1u << e) - 1u;
-            const int tr = til + __popc(tim & below);
-            if (((ltm >> e) & 1u) || tr < q) {
-              const int pos = base + ltl + __popc(ltm & below) + min(tr, q);
-              if (pos >= P0 && pos < P1) {
-                const int dv = c.fromg ? (int)__ldcg(c.D + j + e) : (int)c.D[j + e];
-                emit(pos, c.tok0 + j + e, dv);
-              }
-            }
-          }
-          lt_b += tot & 0xffff;
-          ti_b += tot >> 16;
-        }
-      }
-    }
-  }
-}
-
 template <typename T, int W, int GT, int D_HEAD>
 __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __grid_constant__ DecodeParams p) {
   constexpr int J = planes_for_group(GT);
@@ -165,7 +114,8 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
   constexpr int NSL = AttnState<GT, D_HEAD>::NSL;
   extern __shared__ __align__(1024) uint8_t smem[];
   HATA_TRACE(31);
-  if (p.dbg & 4) return;                                           // diagnostics: launch cost only
+  HATA_CLK(23);
+  if (HATA_DIAG && (p.dbg & 4)) return;                            // diagnostics: launch cost only
 
   const int M = p.M;
   const int NST = p.stages;
@@ -181,8 +131,9 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
   T* Ws = reinterpret_cast<T*>(smem + L.W);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.bars);  // [NST] ring, [NST] W, [NST+1] exchange, [NST+2] partials
   uint32_t* hist = reinterpret_cast<uint32_t*>(smem + L.hist);
-  uint16_t* Dglob = p.ws_D ? p.ws_D + ((int64_t)u * M + r) * p.chunk : nullptr;
+  uint16_t* Dglob = p.ws_D ? p.ws_D + ((int64_t)u * M + r) * dec_dchunk(p.chunk) : nullptr;
   uint16_t* Dloc = p.d_smem ? reinterpret_cast<uint16_t*>(smem + L.D) : Dglob;
+  uint16_t* Ds = reinterpret_cast<uint16_t*>(smem + L.D);          // Dloc when d_smem (shared-space stores)
   float* qf = reinterpret_cast<float*>(smem + L.qf);
   uint32_t* qw = reinterpret_cast<uint32_t*>(smem + L.qw);
   uint32_t* planes = reinterpret_cast<uint32_t*>(smem + L.planes);   // [2][4][8]
@@ -203,8 +154,10 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
   const bool append = p.k_new != nullptr;
   T* qraw = reinterpret_cast<T*>(smem + L.qraw);                    // [G (+1 key)][d] as stored
 
-  // ---- phase 0: start every stream: the code chunk by a few large bulk copies
-  // (TMA), W_g / q / the new key by coalesced 16-byte loads of all threads
+  // ---- phase 0: start every stream with bulk copies (TMA), in the order they
+  // are needed: W_g, q and the new key (they gate the q-hash), then the code
+  // chunk in a few large copies.  A CTA's TMA requests are served in issue
+  // order, so the small copies are not queued behind the 128 KB stream.
   auto issue_stage = [&](int s) {
     const int slot = s % NST;
     const int ntok = min(STAGE_TOK, Lcopy - s * STAGE_TOK);
@@ -213,48 +166,32 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
     if (bytes) bulk_g2s(ring + slot * DEC_STAGE_BYTES, cbase + (t0 + (int64_t)s * STAGE_TOK) * W, bytes, &bars[slot]);
   };
   const int64_t n = p.n[b];                                         // requested before the streams
-  const int wrow = p.rbits * EB;                                    // bytes of one W row
-  const int WROWB = dec_wrow_stride(p.rbits, EB);                   // padded smem row (bank spread)
-  {
-    constexpr int MAXC = 8;                                          // 16-byte chunks per thread (<= 64 KB)
-    const uint4* wsrc = reinterpret_cast<const uint4*>(reinterpret_cast<const T*>(p.Wh) + (int64_t)g * p.d * p.rbits);
-    const int cpr = wrow / 16, nwc = D_HEAD * cpr;                 // chunks per row / in W_g
-    uint4 v[MAXC];
-    // W_g beyond MAXC chunks per thread (fp32 with rbits = 256): earlier batches
-    for (int base = 0; base + MAXC * DEC_THREADS < nwc; base += MAXC * DEC_THREADS) {
-#pragma unroll
-      for (int c = 0; c < MAXC; ++c) v[c] = __ldg(wsrc + base + tid + c * DEC_THREADS);
-#pragma unroll
-      for (int c = 0; c < MAXC; ++c) {
-        const int i = base + tid + c * DEC_THREADS;
-        *reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(Ws) + (i / cpr) * WROWB + (i % cpr) * 16) = v[c];
-      }
+  const int WROWB = dec_wrow_stride(p.rbits, EB);                   // padded smem row of W_g
+  const uint32_t wrow = (uint32_t)(p.rbits * EB);                  // bytes of one W_g row
+  if (tid == 0) {
+    // [0, NST) code ring, NST: W_g + q + k_new, NST+1: spare, NST+2: spare,
+    // NST+3: attention gather batches
+    for (int s = 0; s < NST + 4; ++s) mbar_init(&bars[s], 1);
+    fence_mbar_init();
+    const uint32_t qbytes = (uint32_t)(G * D_HEAD * EB), kbytes = append ? (uint32_t)(D_HEAD * EB) : 0u;
+    mbar_arrive_expect_tx(&bars[NST], D_HEAD * wrow + qbytes + 2 * kbytes);
+    bulk_g2s(qraw, qg, qbytes, &bars[NST]);
+    if (kbytes) {                                                   // new key and value rows
+      bulk_g2s(qraw + G * D_HEAD, reinterpret_cast<const T*>(p.k_new) + (int64_t)u * D_HEAD, kbytes, &bars[NST]);
+      bulk_g2s(qraw + (G + 1) * D_HEAD, reinterpret_cast<const T*>(p.v_new) + (int64_t)u * D_HEAD, kbytes, &bars[NST]);
     }
-    const int wlast = (nwc - 1) / (MAXC * DEC_THREADS) * (MAXC * DEC_THREADS);   // last batch
-#pragma unroll
-    for (int c = 0; c < MAXC; ++c)
-      if (wlast + tid + c * DEC_THREADS < nwc) v[c] = __ldg(wsrc + wlast + tid + c * DEC_THREADS);
-    const int nq = G * D_HEAD * EB / 16, nk = append ? D_HEAD * EB / 16 : 0;
-    uint4 vq = make_uint4(0, 0, 0, 0);
-    const uint4* qsrc = reinterpret_cast<const uint4*>(qg);
-    const uint4* ksrc = reinterpret_cast<const uint4*>(reinterpret_cast<const T*>(p.k_new) + (int64_t)u * D_HEAD);
-    if (tid < nq) vq = __ldg(qsrc + tid);
-    else if (tid < nq + nk) vq = __ldg(ksrc + (tid - nq));
-    // the small loads above are in flight ahead of the 128 KB code stream
-    if (tid == 0) {
-      // [0, NST) code ring, NST: unused, NST+1: exchange + D staging, NST+2: partials,
-      // NST+3: attention gather batches
-      for (int s = 0; s < NST + 4; ++s) mbar_init(&bars[s], 1);
-      fence_mbar_init();
-      for (int s = 0; s < NST && s < nstages; ++s) issue_stage(s);
-    }
-#pragma unroll
-    for (int c = 0; c < MAXC; ++c) {
-      const int i = wlast + tid + c * DEC_THREADS;
-      if (i < nwc) *reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(Ws) + (i / cpr) * WROWB + (i % cpr) * 16) = v[c];
-    }
-    if (tid < nq + nk) reinterpret_cast<uint4*>(qraw)[tid] = vq;
   }
+  __syncthreads();                                                  // barriers initialised
+  {
+    // W_g row by row into padded smem rows (conflict-free ldmatrix), the
+    // requests spread over all warps (bulk-copy issue is serial per warp)
+    const T* wsrc = reinterpret_cast<const T*>(p.Wh) + (int64_t)g * D_HEAD * p.rbits;
+    for (int row = lane * DEC_WARPS + warp; row < D_HEAD; row += DEC_THREADS)
+      bulk_g2s(reinterpret_cast<uint8_t*>(Ws) + row * WROWB, wsrc + (int64_t)row * p.rbits, wrow, &bars[NST]);
+  }
+  __syncthreads();                                                  // W_g requests ahead of the stream
+  if (tid == 0)
+    for (int s = 0; s < NST && s < nstages; ++s) issue_stage(s);
   for (int i = tid; i < p.nbins; i += DEC_THREADS) hist[i] = 0;
   const int kp = (int)(n < (int64_t)p.k ? n : (int64_t)p.k);      // k' = min(k, n)  (R10)
   auto chunk_len = [&](int rr) -> int {                            // valid tokens of rank rr
@@ -271,18 +208,10 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
   const int64_t pos = n - 1;
   const bool owner = append && n >= 1 && pos >= t0 && pos < t0 + Lr;
   const int NV = G + (owner ? 1 : 0);                                // projected vectors
-  __syncthreads();                                                  // W_g, q, k_new in smem
+  mbar_wait(&bars[NST], 0);                                         // W_g, q, k_new in smem
   HATA_TRACE(9);
-  for (int i = tid; i < NV * D_HEAD; i += DEC_THREADS) qf[(i / D_HEAD) * QS + i % D_HEAD] = Elem<T>::to_f(qraw[i]);
-  if (owner) {
-    const T* vn = reinterpret_cast<const T*>(p.v_new) + (int64_t)u * D_HEAD;
-    T* Kd = const_cast<T*>(reinterpret_cast<const T*>(p.K)) + (int64_t)b * p.kv_sb + (int64_t)g * p.kv_sh + pos * p.kv_st;
-    T* Vd = const_cast<T*>(reinterpret_cast<const T*>(p.V)) + (int64_t)b * p.kv_sb + (int64_t)g * p.kv_sh + pos * p.kv_st;
-    for (int i = tid; i < D_HEAD; i += DEC_THREADS) {
-      Kd[i] = qraw[G * D_HEAD + i];                                    // Alg. 3 line 3
-      Vd[i] = vn[i];                                                   // Alg. 3 line 4
-    }
-  }
+  if constexpr (EB != 2)                                            // fp32 paths read q as floats
+    for (int i = tid; i < NV * D_HEAD; i += DEC_THREADS) qf[(i / D_HEAD) * QS + i % D_HEAD] = Elem<T>::to_f(qraw[i]);
   __syncthreads();
   HATA_TRACE(8);
   if constexpr (EB == 2) {
@@ -296,18 +225,11 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
       float c[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
       for (int k0 = 0; k0 < D_HEAD; k0 += 16) {
-        uint32_t a[4];
-        const float* x0 = qf + gid * QS + k0 + 2 * tig;
-        const float* x1 = qf + (gid + 8) * QS + k0 + 2 * tig;
-        const float2 z = make_float2(0.f, 0.f);
-        const float2 f0 = gid < NV ? *reinterpret_cast<const float2*>(x0) : z;
-        const float2 f1 = gid + 8 < NV ? *reinterpret_cast<const float2*>(x1) : z;
-        const float2 f2 = gid < NV ? *reinterpret_cast<const float2*>(x0 + 8) : z;
-        const float2 f3 = gid + 8 < NV ? *reinterpret_cast<const float2*>(x1 + 8) : z;
-        a[0] = pack_bf16x2(f0.x, f0.y);                             // exact: q, k are bf16
-        a[1] = pack_bf16x2(f1.x, f1.y);
-        a[2] = pack_bf16x2(f2.x, f2.y);
-        a[3] = pack_bf16x2(f3.x, f3.y);
+        // A fragment straight from the bf16 rows as stored (adjacent pairs)
+        const uint32_t* x0 = reinterpret_cast<const uint32_t*>(qraw + gid * D_HEAD + k0 + 2 * tig);
+        const uint32_t* x1 = reinterpret_cast<const uint32_t*>(qraw + (gid + 8) * D_HEAD + k0 + 2 * tig);
+        const uint32_t a[4] = {gid < NV ? x0[0] : 0u, gid + 8 < NV ? x1[0] : 0u, gid < NV ? x0[4] : 0u,
+                               gid + 8 < NV ? x1[4] : 0u};
         uint32_t b0, b1;
         ldsm_x2_trans(b0, b1, reinterpret_cast<const uint8_t*>(Ws) + (k0 + (lane & 15)) * WROWB + nt * 16);
         mma_bf16_16816(c, a, b0, b1);
@@ -364,7 +286,9 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
       if (lane == 0) qw[h * W + bb / 32] = word;
     }
   }
+  HATA_TRACE(24);
   __syncthreads();
+  HATA_TRACE(25);
   // publish the query codes (optional output) and the new key's code (Alg. 3 line 9)
   for (int i = tid; i < NV * W; i += DEC_THREADS) {
     const int h = i / W, w = i % W;
@@ -384,6 +308,7 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
       if (lane == 0) { planes[j * 8 + warp] = a; planes[32 + j * 8 + warp] = bb; }
     }
   }
+  HATA_TRACE(26);
   __syncthreads();
   uint32_t A[J][W], Bp[J][W];
 #pragma unroll
@@ -393,7 +318,6 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
 
   HATA_TRACE(1);
   // ---- phase 2: Hamming score + GQA sum (Alg. 3 lines 10-11) + histogram
-  const bool mirror = (M > 1) && p.d_smem;          // D also needed by the other ranks
   auto smem_code = [&](const uint32_t* st, int j, uint32_t (&kc)[W]) {
     if constexpr (W == 4) {
       const uint4 v = reinterpret_cast<const uint4*>(st)[j];
@@ -418,19 +342,33 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
     const int npairs = max(0, min(nval, copied)) / 2;
     const uint32_t* st = reinterpret_cast<const uint32_t*>(ring + slot * DEC_STAGE_BYTES);
     uint32_t* dst = reinterpret_cast<uint32_t*>(Dloc + base);
-    uint32_t* dst2 = mirror ? reinterpret_cast<uint32_t*>(Dglob + base) : nullptr;
-    // two tokens per thread per iteration -> one 32-bit store of a u16 pair
-    for (int j2 = tid; j2 < npairs; j2 += DEC_THREADS) {
-      uint32_t k0[W], k1[W];
+    uint32_t* dsts = reinterpret_cast<uint32_t*>(Ds + base);        // same, as a shared-space pointer
+    // two token pairs per thread per iteration (independent chains for ILP);
+    // a pair -> one 32-bit store of two u16 distances
+    for (int j2 = tid; j2 < npairs; j2 += 2 * DEC_THREADS) {
+      const int j2b = j2 + DEC_THREADS;
+      const bool two = j2b < npairs;
+      uint32_t k0[W], k1[W], k2[W], k3[W];
       smem_code(st, 2 * j2, k0);
       smem_code(st, 2 * j2 + 1, k1);
+      if (two) {
+        smem_code(st, 2 * j2b, k2);
+        smem_code(st, 2 * j2b + 1, k3);
+      }
       const uint32_t d0 = group_distance<W, J>(k0, A, Bp);
       const uint32_t d1 = group_distance<W, J>(k1, A, Bp);
+      const uint32_t d2 = group_distance<W, J>(k2, A, Bp);
+      const uint32_t d3 = group_distance<W, J>(k3, A, Bp);
       atomicAdd(&hist[d0], 1u);
       atomicAdd(&hist[d1], 1u);
-      const uint32_t packed = d0 | (d1 << 16);
-      dst[j2] = packed;
-      if (mirror) dst2[j2] = packed;
+      if (p.d_smem) dsts[j2] = d0 | (d1 << 16);
+      else dst[j2] = d0 | (d1 << 16);
+      if (two) {
+        atomicAdd(&hist[d2], 1u);
+        atomicAdd(&hist[d3], 1u);
+        if (p.d_smem) dsts[j2b] = d2 | (d3 << 16);
+        else dst[j2b] = d2 | (d3 << 16);
+      }
     }
     // leftovers: an odd last token, or tokens past the 16-byte-rounded copy
     const int rest = nval - 2 * npairs;
@@ -447,7 +385,6 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
       const uint32_t dv = group_distance<W, J>(kc, A, Bp);
       atomicAdd(&hist[dv], 1u);
       Dloc[base + j] = (uint16_t)dv;
-      if (mirror) Dglob[base + j] = (uint16_t)dv;
     }
     if (recycle) {                                                  // refill the slot just consumed
       __syncthreads();
@@ -467,206 +404,216 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
     hist[Do] -= 1u;
     hist[Dn] += 1u;
     Dloc[jl] = (uint16_t)Dn;
-    if (mirror) Dglob[jl] = (uint16_t)Dn;
   }
+  if (owner) {
+    // Alg. 3 lines 3-4: K/V rows of the new token (from smem), written before
+    // this rank's arrival at the exchange so that every rank's gather sees them
+    constexpr int CH = D_HEAD * EB / 16;
+    if (tid < 2 * CH) {
+      T* dstrow = const_cast<T*>(reinterpret_cast<const T*>(tid < CH ? p.K : p.V)) + (int64_t)b * p.kv_sb +
+                  (int64_t)g * p.kv_sh + pos * p.kv_st;
+      const uint4 v = reinterpret_cast<const uint4*>(qraw + (tid < CH ? G : G + 1) * D_HEAD)[tid % CH];
+      reinterpret_cast<uint4*>(dstrow)[tid % CH] = v;
+      asm volatile("fence.proxy.async.global;" ::: "memory");        // this rank's own gather reads it by TMA
+    }
+  }
+  // pad D past the valid tokens with 0x7fff (never selected) up to the
+  // selection's per-thread blocking (dec_dchunk)
+  for (int i = Lr + tid; i < dec_dchunk(Lr); i += DEC_THREADS) Dloc[i] = 0x7fffu;
   __syncthreads();
 
   // ---- phase 3: exact top-k' (Alg. 3 lines 12-13) by counting select.
   // thr = D of the k'-th best token; every D < thr is selected; ties at thr
-  // are taken lowest index first (R8) through per-rank quotas in rank (=
-  // token) order.  The ranks of a unit exchange histograms exactly once.
-  const int hs = dec_hist_stride(p.nbins);                          // 16-byte rows
-  int32_t* hm = reinterpret_cast<int32_t*>(smem + L.hm);           // [M][hs]  (ring+W area)
+  // are taken lowest index first (R8): rank by rank (= token order), and in
+  // token order inside a rank.  Every rank publishes the exclusive prefix
+  // counts of its D histogram (cum_r[i] = #{local D < i}, i = 0..nbins) and
+  // adds them into the unit total; after ONE barrier each rank reads the
+  // total (-> thr) and the other ranks' cum_r[thr], cum_r[thr+1] (-> its tie
+  // quota and the output position of its first selected token), then
+  // compacts its OWN selected tokens in order and attends to them.
+  const int hs = dec_hist_stride(p.nbins + 1);
   unsigned* sync = (M > 1) ? p.ws_sync + 2 * u : nullptr;
   HATA_TRACE(2);
-  if (M > 1) {
-    int32_t* gh = p.ws_hist + ((int64_t)u * M + r) * hs;
-    for (int i = tid; i < p.nbins; i += DEC_THREADS) gh[i] = (int32_t)hist[i];
-    __syncthreads();
-    if (tid == 0) {
-      __threadfence();
-      atomicAdd(sync, 1u);
-    }
-    // While the other ranks finish scoring: warm L2 with the K/V rows this
-    // rank will most likely select (its own tokens below a local estimate of
-    // the threshold), so the gather after the selection hits L2.  A pure
-    // prefetch: the selection itself is decided exactly after the exchange.
-    if (!p.cand_mode && !(p.dbg & 2)) {
-      const int want = (int)(((int64_t)kp * Lr + n - 1) / (n > 0 ? n : 1)) * 9 / 8 + 4;
-      int mysum = 0, tb[5];
-      const int BPT = (p.nbins + DEC_THREADS - 1) / DEC_THREADS, i0 = tid * BPT;
-#pragma unroll
-      for (int q = 0; q < 5; ++q) {
-        tb[q] = (q < BPT && i0 + q < p.nbins) ? (int)hist[i0 + q] : 0;
-        mysum += tb[q];
-      }
-      int total;
-      int cum = block_excl_scan(mysum, misc + 16, total);
-      if (tid == 0) misc[4] = p.nbins;
-      __syncthreads();
-#pragma unroll
-      for (int q = 0; q < 5; ++q) {
-        if (cum < want && cum + tb[q] >= want) misc[4] = i0 + q;
-        cum += tb[q];
-      }
-      __syncthreads();
-      const int test = misc[4];                                     // prefetch tokens with D <= test
-      const __nv_bfloat16* Kb = reinterpret_cast<const __nv_bfloat16*>(p.K) + (int64_t)b * p.kv_sb + (int64_t)g * p.kv_sh;
-      const __nv_bfloat16* Vb = reinterpret_cast<const __nv_bfloat16*>(p.V) + (int64_t)b * p.kv_sb + (int64_t)g * p.kv_sh;
-      for (int j = tid * 8; j < Lr; j += DEC_THREADS * 8) {
-        uint32_t ltm, tim;
-        d_masks(Dloc, !p.d_smem, j, Lr, test + 1, ltm, tim);
-        while (ltm) {
-          const int e = __ffs(ltm) - 1;
-          ltm &= ltm - 1;
-          const int64_t t = t0 + j + e;
-          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(Kb + t * p.kv_st), "r"(D_HEAD * EB) : "memory");
-          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(Vb + t * p.kv_st), "r"(D_HEAD * EB) : "memory");
-        }
-      }
-    }
-    if (tid == 0) {
-      while (ld_acquire_gpu(sync) < (unsigned)M) {
-      }
-      // other ranks' generic-proxy writes -> this thread's async-proxy (bulk copy) reads
-      asm volatile("fence.proxy.async.global;" ::: "memory");
-      const uint32_t bytes = (uint32_t)(M * hs * 4);
-      mbar_arrive_expect_tx(&bars[NST + 1], bytes);
-      bulk_g2s(hm, p.ws_hist + (int64_t)u * M * hs, bytes, &bars[NST + 1]);
-    }
-    mbar_wait(&bars[NST + 1], 0);
-  } else {
-    for (int i = tid; i < p.nbins; i += DEC_THREADS) hm[i] = (int32_t)hist[i];
-    __syncthreads();
-  }
-  HATA_TRACE(3);
-  // (a) per-bin totals over the ranks + block scan -> thr, #below
+  constexpr int BPT_MAX = (8 * 256 + 1 + DEC_THREADS) / DEC_THREADS;  // nbins + 1 <= G*rbits + 2 (G <= 8, rbits <= 256)
+  const int BPT = (p.nbins + DEC_THREADS) / DEC_THREADS;
+  const int i0 = tid * BPT;
+  int tb[BPT_MAX];
+  int cum;
   {
-    constexpr int BPT_MAX = 5;                                       // nbins <= 2560
-    const int BPT = (p.nbins + DEC_THREADS - 1) / DEC_THREADS;
-    const int i0 = tid * BPT;
-    int tb[BPT_MAX];
     int mysum = 0;
 #pragma unroll
     for (int q = 0; q < BPT_MAX; ++q) {
-      tb[q] = 0;
-      const int i = i0 + q;
-      if (q < BPT && i < p.nbins) {
-        int s0 = 0, s1 = 0, s2 = 0, s3 = 0, rr = 0;
-        for (; rr + 4 <= M; rr += 4) {
-          s0 += hm[rr * hs + i]; s1 += hm[(rr + 1) * hs + i]; s2 += hm[(rr + 2) * hs + i]; s3 += hm[(rr + 3) * hs + i];
-        }
-        for (; rr < M; ++rr) s0 += hm[rr * hs + i];
-        tb[q] = s0 + s1 + s2 + s3;
-      }
+      tb[q] = (q < BPT && i0 + q < p.nbins) ? (int)hist[i0 + q] : 0;
       mysum += tb[q];
     }
     int total;
-    int cum = block_excl_scan(mysum, misc + 16, total);
-    if (tid == 0 && kp <= 0) { misc[0] = -1; misc[1] = 0; }
+    cum = block_excl_scan(mysum, misc + 16, total);                  // #{local D < i0}
+  }
+  if (tid == 0) { misc[0] = -1; misc[1] = 0; misc[4] = p.nbins; }
+  if (M > 1) {
+    int32_t* gc = p.ws_hist + ((int64_t)u * M + r) * hs;
+    int32_t* gt = p.ws_tot + (int64_t)u * hs;
+    int c = cum;
 #pragma unroll
     for (int q = 0; q < BPT_MAX; ++q) {
-      if (q < BPT && i0 + q < p.nbins && kp > 0 && cum < kp && cum + tb[q] >= kp) {
-        misc[0] = i0 + q;          // thr
-        misc[1] = kp - cum;        // need: ties to take at thr
+      const int i = i0 + q;
+      if (q < BPT && i <= p.nbins) {
+        gc[i] = c;
+        if (c) atomicAdd(gt + i, c);
       }
-      cum += tb[q];
+      c += tb[q];
+    }
+    __syncthreads();
+    if (tid == 0) red_add_release_gpu(sync, 1u);   // release the CTA's writes (cumulative over bar.sync)
+    HATA_TRACE(27);
+    if (tid == 0) {
+      while (ld_acquire_gpu(sync) < (unsigned)M) {
+      }
+      // the owner's K/V row (generic stores) -> this CTA's gather (async proxy)
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+    }
+    __syncthreads();
+    HATA_TRACE(3);
+    // thr: the bin where the unit's cumulative count crosses k'
+#pragma unroll
+    for (int q = 0; q < BPT_MAX; ++q) {
+      const int i = i0 + q;
+      if (q < BPT && i < p.nbins && kp > 0) {
+        const int a = __ldcg(gt + i), z = __ldcg(gt + i + 1);
+        if (a < kp && kp <= z) { misc[0] = i; misc[1] = kp - a; }
+      }
+    }
+  } else {
+    HATA_TRACE(3);
+    int c = cum;
+#pragma unroll
+    for (int q = 0; q < BPT_MAX; ++q) {
+      if (q < BPT && i0 + q < p.nbins && kp > 0 && c < kp && kp <= c + tb[q]) { misc[0] = i0 + q; misc[1] = kp - c; }
+      c += tb[q];
     }
   }
   __syncthreads();
-  HATA_TRACE(11);
   const int thr = misc[0];
   const int need = misc[1];
-  // (b) per-rank #(D < thr) and #(D == thr): warp per rank
-  int32_t* rb_below = red;                       // [M]
-  int32_t* rb_ties = red + DEC_MAX_RANKS;        // [M]
-  int32_t* rb_off = red + 2 * DEC_MAX_RANKS;     // [M]
-  int32_t* rb_quota = red + 3 * DEC_MAX_RANKS;   // [M]
-  for (int rr = warp; rr < M; rr += DEC_WARPS) {
-    int s0 = 0, s1 = 0, s2 = 0, s3 = 0, i = lane;
-    for (; i + 96 < thr; i += 128) {
-      s0 += hm[rr * hs + i]; s1 += hm[rr * hs + i + 32]; s2 += hm[rr * hs + i + 64]; s3 += hm[rr * hs + i + 96];
-    }
-    for (; i < thr; i += 32) s0 += hm[rr * hs + i];
-    const int s = warp_sum_i(s0 + s1 + s2 + s3);
-    if (lane == 0) { rb_below[rr] = s; rb_ties[rr] = thr >= 0 ? hm[rr * hs + thr] : 0; }
+  // this rank's tie quota and the selection position of its first token
+  // (computed by every warp: no further barrier); the loads are issued here
+  // and consumed after the counting pass below
+  int quota = need, off0 = 0;
+  int bl = 0, ti = 0;
+  if (M > 1 && thr >= 0 && lane < M) {
+    const int32_t* cr = p.ws_hist + ((int64_t)u * M + lane) * hs;
+    bl = __ldcg(cr + thr);
+    ti = __ldcg(cr + thr + 1);
   }
-  __syncthreads();
-  // (c) quotas, selection offsets, and staging of the D arrays this rank needs
-  const int R = (kp + M - 1) / M;                                   // equal share of the selection
-  const int P0 = min(kp, r * R), P1 = min(kp, P0 + R);
-  ChunkRef* chref = reinterpret_cast<ChunkRef*>(smem + L.chref);   // [DEC_MAX_RANKS]
-  if (warp == 0) {
-    const int bl = lane < M ? rb_below[lane] : 0, ti = lane < M ? rb_ties[lane] : 0;
+  HATA_TRACE(11);
+  HATA_CLK(0);
+  // order-preserving compaction of this rank's selected tokens.  Thread t
+  // owns the contiguous tokens [8*S8*t, 8*S8*(t+1)) (the D buffer is padded
+  // with 0x7fff to 8*S8*DEC_THREADS, so every load is a full, aligned uint4).
+  // Pass 1 counts (D < thr) and (D == thr) per thread with SIMD half-word
+  // compares, a warp scan + one barrier give each thread its offsets, pass 2
+  // re-reads its tokens and emits the selected ones with predicated,
+  // fully unrolled code (no per-token branches, no warp votes).
+  int32_t* oidx = p.out_idx ? p.out_idx + (int64_t)u * p.k : nullptr;
+  int32_t* osc = p.out_score ? p.out_score + (int64_t)u * p.k : nullptr;
+  int32_t* ocd = p.cand_D ? p.cand_D + (int64_t)u * p.k : nullptr;
+  const int Gr = G * p.rbits;
+  const int S8 = (Lr + 8 * DEC_THREADS - 1) / (8 * DEC_THREADS);   // uint4 (8 tokens) per thread
+  const uint4* Dv = reinterpret_cast<const uint4*>(Dloc) + (int64_t)tid * S8;
+  // SWAR compares on half-words (every D and the pad 0x7fff are < 2^15):
+  // ((x | 0x8000) - d) keeps bit 15 iff d <= x, with no borrow between halves
+  const uint32_t lt_k = thr >= 1 ? (uint32_t)(thr - 1) * 0x10001u + 0x80008000u : 0u;   // d <  thr
+  const uint32_t le_k = thr >= 0 ? (uint32_t)thr * 0x10001u + 0x80008000u : 0u;         // d <= thr
+  auto swar = [&](uint32_t w, uint32_t& ltw, uint32_t& eqw) {
+    ltw = thr >= 1 ? (lt_k - w) & 0x80008000u : 0u;
+    const uint32_t lew = thr >= 0 ? (le_k - w) & 0x80008000u : 0u;
+    eqw = lew & ~ltw;
+  };
+  int lt_m = 0, eq_m = 0;
+  if (thr >= 0) {
+#pragma unroll 4
+    for (int c = 0; c < S8; ++c) {
+      const uint4 x = Dv[c];
+      uint32_t l0, e0, l1, e1, l2, e2, l3, e3;
+      swar(x.x, l0, e0); swar(x.y, l1, e1); swar(x.z, l2, e2); swar(x.w, l3, e3);
+      lt_m += __popc(l0) + __popc(l1) + __popc(l2) + __popc(l3);
+      eq_m += __popc(e0) + __popc(e1) + __popc(e2) + __popc(e3);
+    }
+  }
+  HATA_CLK(1);
+  // warp-inclusive scans of both counts
+  int lt_i = lt_m, eq_i = eq_m;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int a = __shfl_up_sync(0xffffffffu, lt_i, o), e = __shfl_up_sync(0xffffffffu, eq_i, o);
+    if (lane >= o) { lt_i += a; eq_i += e; }
+  }
+  int* wcnt = misc + 16;                                            // [DEC_WARPS][2] warp totals
+  if (lane == 31) { wcnt[2 * warp] = lt_i; wcnt[2 * warp + 1] = eq_i; }
+  HATA_CLK(2);
+  HATA_TRACE(18);
+  if (M > 1 && thr >= 0) {
+    ti -= bl;
     int incl = ti;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const int v = __shfl_up_sync(0xffffffffu, incl, o);
       if (lane >= o) incl += v;
     }
-    const int quota = max(0, min(need - (incl - ti), ti));
-    const int sel = bl + quota;
+    const int qv = max(0, min(need - (incl - ti), ti));
+    const int sel = bl + qv;
     int inc2 = sel;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const int v = __shfl_up_sync(0xffffffffu, inc2, o);
       if (lane >= o) inc2 += v;
     }
-    const int off = inc2 - sel;
-    if (lane < M) { rb_quota[lane] = quota; rb_off[lane] = off; }
-    // chunks whose selections overlap [P0, P1): a contiguous run of ranks
-    const bool ov = lane < M && P1 > P0 && sel > 0 && off < P1 && off + sel > P0;
-    const uint32_t ovm = __ballot_sync(0xffffffffu, ov);
-    const bool own = lane == r && p.d_smem;
-    const int Lc = lane < M ? chunk_len(lane) : 0;
-    uint32_t bytes = (ov && !own) ? (uint32_t)((Lc * 2 + 15) & ~15) : 0u;
-    // smem slots after the histograms, in rank order
-    uint32_t slot = (bytes + 127) & ~127u, sx = slot;
+    quota = __shfl_sync(0xffffffffu, qv, r);
+    off0 = __shfl_sync(0xffffffffu, inc2 - sel, r);
+  }
+  HATA_CLK(3);
+  __syncthreads();
+  HATA_CLK(4);
+  // this thread's exclusive offsets within the rank, and the rank totals
+  int lt_b = lt_i - lt_m, ti_b = eq_i - eq_m, lt_tot = 0, ti_tot = 0;
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t v = __shfl_up_sync(0xffffffffu, sx, o);
-      if (lane >= o) sx += v;
-    }
-    const uint32_t soff = (uint32_t)((M * hs * 4 + 127) & ~127) + sx - slot;
-    if (soff + bytes > (uint32_t)L.sc_limit) bytes = 0;            // does not fit: scan it in L2
-    const uint32_t tx = (uint32_t)warp_sum_i((int)bytes);
-    if (ov) {
-      const int k = __popc(ovm & ((1u << lane) - 1u));
-      ChunkRef c;
-      c.L = Lc;
-      c.quota = quota;
-      c.base = off;
-      c.tok0 = lane * per;
-      c.fromg = (!own && !bytes) ? 1 : 0;
-      c.D = own ? Dloc : (bytes ? reinterpret_cast<const uint16_t*>(smem + soff)
-                                : p.ws_D + ((int64_t)u * M + lane) * p.chunk);
-      chref[k] = c;
-    }
-    if (lane == 0) { misc[2] = __popc(ovm); misc[3] = tx ? 1 : 0; }
-    if (tx) {
-      if (lane == 0) {
-        asm volatile("fence.proxy.async.global;" ::: "memory");     // D written by generic stores
-        mbar_arrive_expect_tx(&bars[NST + 1], tx);
+  for (int w = 0; w < DEC_WARPS; ++w) {
+    const int cl = wcnt[2 * w], ct = wcnt[2 * w + 1];
+    if (w < warp) { lt_b += cl; ti_b += ct; }
+    lt_tot += cl;
+    ti_tot += ct;
+  }
+  const int Rr = lt_tot + min(ti_tot, quota);                       // rows this rank attends to
+  HATA_CLK(5);
+  HATA_TRACE(21);
+  if (thr >= 0 && lt_m + min(max(quota - ti_b, 0), eq_m) > 0) {
+    for (int c = 0; c < S8; ++c) {
+      const uint4 x = Dv[c];
+      uint32_t lw[4], ew[4];
+      swar(x.x, lw[0], ew[0]); swar(x.y, lw[1], ew[1]); swar(x.z, lw[2], ew[2]); swar(x.w, lw[3], ew[3]);
+      if (!((lw[0] | lw[1] | lw[2] | lw[3] | ew[0] | ew[1] | ew[2] | ew[3]))) continue;   // no candidate here
+      const uint32_t wv[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {                                 // tokens in order: word e/2, half e%2
+        const int sh = 15 + 16 * (e & 1);
+        const int lt = (lw[e >> 1] >> sh) & 1, eq = (ew[e >> 1] >> sh) & 1;
+        if (lt || (eq && ti_b < quota)) {
+          const int pl = lt_b + min(ti_b, quota);
+          const int tok = (tid * S8 + c) * 8 + e;
+          rows[pl] = (int32_t)t0 + tok;
+          const int pos = off0 + pl;
+          if (oidx) oidx[pos] = (int32_t)(t0 + tok + p.token_offset);
+          const int dv = (int)((wv[e >> 1] >> (16 * (e & 1))) & 0xffffu);
+          if (osc) osc[pos] = Gr - 2 * dv;                           // S = G*rbits - 2D
+          if (ocd) ocd[pos] = dv;
+        }
+        lt_b += lt;
+        ti_b += eq;
       }
-      __syncwarp();
-      if (bytes) bulk_g2s(smem + soff, p.ws_D + ((int64_t)u * M + lane) * p.chunk, bytes, &bars[NST + 1]);
     }
   }
-  __syncthreads();
-  HATA_TRACE(12);
-  const int nch = misc[2];
-  if (misc[3]) mbar_wait(&bars[NST + 1], M > 1 ? 1 : 0);
-  HATA_TRACE(4);
-  int32_t* oidx = p.out_idx ? p.out_idx + (int64_t)u * p.k : nullptr;
-  int32_t* osc = p.out_score ? p.out_score + (int64_t)u * p.k : nullptr;
-  int32_t* ocd = p.cand_D ? p.cand_D + (int64_t)u * p.k : nullptr;
-  const int Gr = G * p.rbits;
-  scan_chunks(chref, nch, thr, P0, P1, misc + 32, [&](int pos, int tok, int Dv) {
-    rows[pos - P0] = tok;
-    if (oidx) oidx[pos] = (int32_t)(tok + p.token_offset);
-    if (osc) osc[pos] = Gr - 2 * Dv;                               // S = G*rbits - 2D
-    if (ocd) ocd[pos] = Dv;
-  });
+  HATA_CLK(6);
+  HATA_TRACE(22);
   if (r == 0) {
     for (int i = kp + tid; i < p.k; i += DEC_THREADS) {
       if (oidx) oidx[i] = -1;
@@ -686,11 +633,11 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
     const T* Kb = reinterpret_cast<const T*>(p.K) + (int64_t)b * p.kv_sb + (int64_t)g * p.kv_sh;
     const T* Vb = reinterpret_cast<const T*>(p.V) + (int64_t)b * p.kv_sb + (int64_t)g * p.kv_sh;
     if constexpr (EB == 2) {
-      attend_rows_mma<GT, D_HEAD>(rows, P1 - P0, Kb, Vb, p.kv_st, qf, G, p.scale, smem + L.kv, p.rows_cap, L.rb,
+      attend_rows_mma<GT, D_HEAD>(rows, Rr, Kb, Vb, p.kv_st, reinterpret_cast<const __nv_bfloat16*>(qraw), G, p.scale, smem + L.kv, p.rows_cap, L.rb,
                                   m_s, l_s, st, &bars[NST + 3], p.trace);
     } else {
       float* sc = reinterpret_cast<float*>(smem + L.sc);
-      attend_rows<T, GT, D_HEAD>(rows, P1 - P0, Kb, Vb, p.kv_st, qf, G, p.scale, smem + L.kv, sc, p.rows_cap, L.rb,
+      attend_rows<T, GT, D_HEAD>(rows, Rr, Kb, Vb, p.kv_st, qf, G, p.scale, smem + L.kv, sc, p.rows_cap, L.rb,
                                  m_s, l_s, corr_s, st);
     }
   }
@@ -727,69 +674,52 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
     for (int s = 0; s < NSL; ++s) {
       const int sl = tid + s * DEC_THREADS;
       const int h = sl / (D_HEAD / 2), e2 = sl % (D_HEAD / 2);
-      if (h < G) { mypart[h * PS + 2 + 2 * e2] = st.acc[s][0]; mypart[h * PS + 3 + 2 * e2] = st.acc[s][1]; }
+      if (h < G) *reinterpret_cast<float2*>(mypart + h * PS + 2 + 2 * e2) = make_float2(st.acc[s][0], st.acc[s][1]);
     }
     if (tid < G) { mypart[tid * PS] = m_s[tid]; mypart[tid * PS + 1] = l_s[tid]; }
   }
   __syncthreads();
   if (tid == 0) {
-    __threadfence();
-    const unsigned prev = atomicAdd(sync + 1, 1u);
+    // release this partial (cumulative over bar.sync), acquire the others'
+    const unsigned prev = atom_add_acq_rel_gpu(sync + 1, 1u);
     misc[2] = (prev == (unsigned)(M - 1));
   }
   __syncthreads();
   HATA_TRACE(15);
   if (!misc[2]) return;
-  // last rank: every partial is visible (writer fence + counter); pull them
-  // into smem with one bulk copy, then merge in rank order
+  // last rank: every partial is visible (writer fence + counter); merge them
+  // in rank order straight from L2 (thread = one output element)
   if (!p.cand_mode) {
-    float* sp = reinterpret_cast<float*>(smem);                      // ring+W area is free
-    float* wgt = reinterpret_cast<float*>(smem + L.hm + ((M * PB * 4 + 127) & ~127));   // [M][GT] weights
-    if (tid == 0) {
-      __threadfence();
-      HATA_TRACE(24);
-      asm volatile("fence.proxy.async.global;" ::: "memory");
-      const uint32_t bytes = (uint32_t)(M * PB * 4);
-      mbar_arrive_expect_tx(&bars[NST + 2], bytes);
-      bulk_g2s(sp, p.ws_part + (int64_t)u * M * PB, bytes, &bars[NST + 2]);
-      HATA_TRACE(25);
-    }
-    mbar_wait(&bars[NST + 2], 0);
-    HATA_TRACE(26);
-    // per-head max, then per-(rank, head) weights e^{m_r - M_h}, then L_h
-    if (tid < G) {
-      float Mx = -INFINITY;
-      for (int rr = 0; rr < M; ++rr) Mx = fmaxf(Mx, sp[rr * PB + tid * PS]);
-      m_s[tid] = Mx;
-    }
-    __syncthreads();
-    for (int t = tid; t < M * G; t += DEC_THREADS) {
-      const int rr = t / G, h = t % G;
-      const float mr = sp[rr * PB + h * PS];
-      wgt[rr * GT + h] = (mr == -INFINITY) ? 0.f : expf(mr - m_s[h]);
-    }
-    __syncthreads();
-    if (tid < G) {
-      float Ls = 0.f;
-      for (int rr = 0; rr < M; ++rr) Ls = fmaf(sp[rr * PB + tid * PS + 1], wgt[rr * GT + tid], Ls);
-      l_s[tid] = Ls;
-    }
-    __syncthreads();
+    // a warp's 32 outputs share the head h (D_HEAD % 32 == 0): lane rr holds
+    // rank rr's (m, l) and merge weight; every load below is independent
+    const float* part = p.ws_part + (int64_t)u * M * PB;
+    static_assert(D_HEAD % 32 == 0, "warp = one head");
     for (int o = tid; o < G * D_HEAD; o += DEC_THREADS) {
       const int h = o / D_HEAD, e = o % D_HEAD;
-      float a0 = 0.f, a1 = 0.f;
-      int rr = 0;
-      for (; rr + 2 <= M; rr += 2) {
-        a0 = fmaf(sp[rr * PB + h * PS + 2 + e], wgt[rr * GT + h], a0);
-        a1 = fmaf(sp[(rr + 1) * PB + h * PS + 2 + e], wgt[(rr + 1) * GT + h], a1);
-      }
-      if (rr < M) a0 = fmaf(sp[rr * PB + h * PS + 2 + e], wgt[rr * GT + h], a0);
-      const float Ls = l_s[h];
-      store_out(h, e, Ls > 0.f ? (a0 + a1) / Ls : 0.f);
+      const float mr = lane < M ? __ldcg(part + lane * PB + h * PS) : -INFINITY;
+      const float lr = lane < M ? __ldcg(part + lane * PB + h * PS + 1) : 0.f;
+      float Mx = mr;
+#pragma unroll
+      for (int x = 16; x > 0; x >>= 1) Mx = fmaxf(Mx, __shfl_xor_sync(0xffffffffu, Mx, x));
+      const float w = (mr == -INFINITY) ? 0.f : expf(mr - Mx);
+      float Ls = lr * w;
+#pragma unroll
+      for (int x = 16; x > 0; x >>= 1) Ls += __shfl_xor_sync(0xffffffffu, Ls, x);
+      float v[DEC_MAX_RANKS];                                        // every load in flight at once
+#pragma unroll
+      for (int i = 0; i < DEC_MAX_RANKS; ++i) v[i] = i < M ? __ldcg(part + i * PB + h * PS + 2 + e) : 0.f;
+      float a0 = 0.f;
+#pragma unroll
+      for (int i = 0; i < DEC_MAX_RANKS; ++i) a0 = fmaf(v[i], __shfl_sync(0xffffffffu, w, i), a0);   // rank order
+      store_out(h, e, Ls > 0.f ? a0 / Ls : 0.f);
     }
   }
-  if (tid == 0) { sync[0] = 0u; sync[1] = 0u; }     // leave the workspace zeroed for the next launch
+  // leave the workspace zeroed for the next launch (every rank has read the
+  // unit total before publishing its partial)
+  for (int i = tid; i <= p.nbins; i += DEC_THREADS) p.ws_tot[(int64_t)u * hs + i] = 0;
+  if (tid == 0) { sync[0] = 0u; sync[1] = 0u; }
   HATA_TRACE(7);
+  HATA_CLK(14);
 }
 
 }  // namespace hata

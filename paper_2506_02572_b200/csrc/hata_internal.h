@@ -38,7 +38,7 @@ cudaError_t launch_hash_keys_tc(const HashKeysParams& p, cudaStream_t s);
 struct DecodePlan {
   int M, stages, chunk, R_cap, rows_cap, nbins, GT, smem;
   bool d_smem, rows_global;
-  size_t ws_sync, ws_hist, ws_part, ws_D, ws_rows, ws_total;   // workspace byte offsets / size
+  size_t ws_sync, ws_hist, ws_tot, ws_part, ws_D, ws_rows, ws_total;   // workspace byte offsets / size
 };
 struct DecodeParams;
 DecodePlan plan_decode(int B, int Hq, int Hkv, int d, int rbits, int64_t n_max, int k, int elem_bytes);

@@ -10,6 +10,8 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
+os.environ.setdefault("HATA_LIB", "libhata_trace.so")   # the build with the phase stamps compiled in
+
 import torch  # noqa: E402
 
 import bench  # noqa: E402
@@ -17,9 +19,9 @@ import synth  # noqa: E402
 
 NAMES = {31: "kernel_entry", 0: "start", 1: "hash_done", 2: "score_done", 3: "hist_x", 4: "D_staged", 5: "select_done",
          6: "attn_done", 7: "end(last)", 8: "qk_loaded", 9: "W_ready", 10: "stage0", 11: "thr",
-         12: "quota", 13: "last_stage", 14: "unused14", 15: "published", 16: "kv_gathered",
+         12: "quota", 13: "last_stage", 14: "sel_pass1_done", 15: "published", 16: "kv_gathered",
          17: "groups_done", 19: "kv_issued", 20: "kv_gathered_1st", 21: "groups_done_1st",
-         23: "kv_issued_1st", 20: "attn_entry", 24: "c_fenced", 25: "c_copy_issued", 26: "c_copied"}
+         23: "kv_issued_1st", 20: "attn_entry", 27: "arrived", 28: "prefetched", 18: "sel_counted", 21: "sel_scanned", 22: "sel_emitted", 29: "attn_wmerge1", 30: "attn_wmerge2", 24: "hash_mma_done(t0)", 25: "hash_synced", 26: "planes_done(t0)"}
 
 
 def main():
@@ -28,11 +30,11 @@ def main():
     fused = (sys.argv[3] != "0") if len(sys.argv) > 3 else True
     sh = synth.CONFIGS[cfg]
     dev = torch.device("cuda", 0)
-    sets = [bench.Step(sh, 2000 + i, dev) for i in range(8)]
+    sets = [bench.Step(sh, 2000 + i, dev) for i in range(int(os.environ.get('TRACE_SETS', '8')))]
     H = sets[0].H
     M = H.decode_ranks(sh.B, sh.Hq, sh.Hkv, sh.d, sh.rbits, sh.N, sh.k, sets[0].K.dtype)
     nct = M * sh.B * sh.Hkv
-    buf = torch.zeros(nct * 32, dtype=torch.int64, device=dev)
+    buf = torch.zeros(nct * 64, dtype=torch.int64, device=dev)
     for s in sets:
         s.run()
     torch.cuda.synchronize()
@@ -47,18 +49,40 @@ def main():
         (s.run if fused else s.decode)()
         H.lib().hata_debug_timestamp(marks.data_ptr() + 8, st)        # decode kernel done
         torch.cuda.synchronize()
-        t = buf.view(nct, 32).cpu().double()
+        t = buf.view(nct, 64).cpu().double()
         mk = marks.cpu().double()
         t0 = mk[0]
         print(f"rep{rep} marker_before=0  decode_done_marker={(mk[1] - t0).item() / 1e3:.2f} us")
         cols = []
+        last = (t[:, 7] > 0)
+        if last.any():
+            cyc = (t[last, 32 + 14] - t[last, 32 + 23]).median().item()
+            ns = (t[last, 7] - t[last, 31]).median().item()
+            print(f"rep{rep} clock: {cyc:.0f} cycles over {ns:.0f} ns -> {cyc / max(ns, 1):.3f} GHz (last ranks)")
         for i in range(32):
+            pass
             c = t[:, i]
             c = c[c > 0]
             if len(c):
                 c = (c - t0) / 1e3
                 cols.append((c.median().item(), c.max().item(), NAMES.get(i, str(i))))
         cols.sort()
+        ck = t[:, 32:]
+        names = ["count_start", "count_loop", "warp_sums", "quota(bl/ti)", "sync", "offsets", "emit"]
+        seg = []
+        for i in range(1, 7):
+            a_, b_ = ck[:, i - 1], ck[:, i]
+            ok = (a_ > 0) & (b_ > 0)
+            if ok.any():
+                seg.append(f"{names[i]}={(b_[ok] - a_[ok]).median().item():.0f}")
+        if seg:
+            print(f"rep{rep} select cycles (t0 warp): " + " ".join(seg))
+        for i in (8, 27, 5, 20, 15):
+            c = t[:, i]
+            if (c > 0).any():
+                j = int(torch.argmax(c).item())
+                print(f"rep{rep} slowest at {NAMES.get(i, i)}: cta {j} (rank {j % M}, unit {j // M}) "
+                      f"+{(c[j] - c[c > 0].median()).item() / 1e3:.2f} us over median")
         print(f"rep{rep} " + " ".join(f"{nm}={md:.2f}/{mx:.2f}" for md, mx, nm in cols))
     H._lib.check(H.lib().hata_debug_trace(None), "trace off")
 
