@@ -66,12 +66,12 @@ def test_validation_rejects_before_launch(lib):
 def test_workspace_query(lib):
     from paper_2506_02572_b200 import decode_ranks, decode_workspace_size
     # CFG-4: 8 (b, g) units x M=18 ranks on a 148-SM part; the ranks exchange
-    # histograms and D arrays through the workspace
+    # prefix counts of their histograms (513 bins + 1) and flash-decoding
+    # partials (G heads x (d + 2) floats) through the workspace
     M = decode_ranks(1, 32, 8, 128, 128, 131072, 2048)
     assert M == 18
     ws = decode_workspace_size(1, 32, 8, 128, 128, 131072, 2048)
-    chunk = -(-131072 // M // 64) * 64
-    assert ws >= 8 * M * (chunk * 2 + 513 * 4)
+    assert ws >= 8 * M * (514 * 4 + 4 * 130 * 4)
     # one rank per unit (128 units): no exchange; D of a 128K chunk spills to the workspace
     assert decode_ranks(16, 32, 8, 128, 128, 131072, 2048) == 1
     assert decode_workspace_size(16, 32, 8, 128, 128, 131072, 2048) >= 128 * 131072 * 2
