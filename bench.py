@@ -43,6 +43,15 @@ def _peaks():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
+def _ncu_traffic(kernel, workload):
+    """DRAM bytes per launch from the committed ncu capture (profiles/ncu_traffic.json), else None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            return int(json.load(f)[kernel][workload]["bytes"])
+    except Exception:
+        return None
+
+
 def algorithmic_bytes(sh, N=None, k=None):
     """codes + k' selected K/V rows + q (north_star roofline definition)."""
     N = sh.N if N is None else N
@@ -477,7 +486,8 @@ def main():
                    "l2": f"rotating {N_SETS} distinct cache sets ({N_SETS} x {bytes_step / 1e6:.1f} MB step bytes "
                          f"> 126 MB L2)", "parallelism": "single GPU"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": None, "kernel": "hata_decode_kernel", "algorithmic_bytes_per_launch": bytes_step,
+                     "traffic": _ncu_traffic("hata_decode_kernel", sh.name), "traffic_source": "profiles/ncu_traffic.json (ncu dram__bytes_read+write per launch)",
+                     "kernel": "hata_decode_kernel", "algorithmic_bytes_per_launch": bytes_step,
                      "us_per_launch": us_dec, "peak_source": peak_src,
                      "frac_vs_8TBs": achieved / 8000.0},
         "clocks": r["clocks"],

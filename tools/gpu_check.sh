@@ -10,7 +10,7 @@ tail -15 gpurun_out/pytest_$TAG.log
 timeout 600 python bench.py > gpurun_out/bench_$TAG.json 2> gpurun_out/bench_$TAG.err
 tail -3 gpurun_out/bench_$TAG.err; cat gpurun_out/bench_$TAG.json
 if [ -n "$NCU" ]; then
-timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -c 200 --csv --log-file gpurun_out/launches_$TAG.csv python bench.py --steps 20 --warmup 3 --no-cpu --no-secondary > /dev/null 2>&1
+timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:hata -c 60 --csv --log-file gpurun_out/launches_$TAG.csv python bench.py --steps 20 --warmup 3 --no-cpu --no-secondary > /dev/null 2>&1
 timeout 400 ncu --set full --clock-control none --import-source on -k regex:hata_decode -s 40 -c 1 -o gpurun_out/prof_decode_$TAG python bench.py --steps 10 --warmup 3 --no-cpu --no-secondary > gpurun_out/ncu_$TAG.log 2>&1
 tail -2 gpurun_out/ncu_$TAG.log
 fi
