@@ -591,24 +591,35 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
       const uint4 x = Dv[c];
       uint32_t lw[4], ew[4];
       swar(x.x, lw[0], ew[0]); swar(x.y, lw[1], ew[1]); swar(x.z, lw[2], ew[2]); swar(x.w, lw[3], ew[3]);
-      if (!((lw[0] | lw[1] | lw[2] | lw[3] | ew[0] | ew[1] | ew[2] | ew[3]))) continue;   // no candidate here
-      const uint32_t wv[4] = {x.x, x.y, x.z, x.w};
-#pragma unroll
-      for (int e = 0; e < 8; ++e) {                                 // tokens in order: word e/2, half e%2
-        const int sh = 15 + 16 * (e & 1);
-        const int lt = (lw[e >> 1] >> sh) & 1, eq = (ew[e >> 1] >> sh) & 1;
-        if (lt || (eq && ti_b < quota)) {
-          const int pl = lt_b + min(ti_b, quota);
-          const int tok = (tid * S8 + c) * 8 + e;
+      // 8-bit masks of the block, bit i = token i (word i/2, half i%2)
+      auto pack8 = [](const uint32_t (&m)[4]) -> uint32_t {
+        return ((m[0] >> 15) & 1u) | ((m[0] >> 30) & 2u) | ((m[1] >> 13) & 4u) | ((m[1] >> 28) & 8u) |
+               ((m[2] >> 11) & 16u) | ((m[2] >> 26) & 32u) | ((m[3] >> 9) & 64u) | ((m[3] >> 24) & 128u);
+      };
+      const uint32_t lt8 = pack8(lw), eq8 = pack8(ew);
+      if (lt8 | eq8) {
+        // the first max(0, quota - ti_b) ties of the block are taken (R8)
+        uint32_t tie8 = 0u, e8 = eq8;
+        for (int take = min(__popc(eq8), max(quota - ti_b, 0)); take > 0; --take) {
+          tie8 |= e8 & (0u - e8);                                    // lowest remaining tie
+          e8 &= e8 - 1u;
+        }
+        const uint32_t sel8 = lt8 | tie8;
+        const int base = lt_b + min(ti_b, quota);                    // position of the block's first pick
+        const uint32_t wv[4] = {x.x, x.y, x.z, x.w};
+        for (uint32_t m = sel8; m; m &= m - 1u) {
+          const int i = __ffs(m) - 1;
+          const int pl = base + __popc(sel8 & ((1u << i) - 1u));
+          const int tok = (tid * S8 + c) * 8 + i;
           rows[pl] = (int32_t)t0 + tok;
           const int pos = off0 + pl;
           if (oidx) oidx[pos] = (int32_t)(t0 + tok + p.token_offset);
-          const int dv = (int)((wv[e >> 1] >> (16 * (e & 1))) & 0xffffu);
+          const int dv = (int)((wv[i >> 1] >> (16 * (i & 1))) & 0xffffu);
           if (osc) osc[pos] = Gr - 2 * dv;                           // S = G*rbits - 2D
           if (ocd) ocd[pos] = dv;
         }
-        lt_b += lt;
-        ti_b += eq;
+        lt_b += __popc(lt8);
+        ti_b += __popc(eq8);
       }
     }
   }
@@ -679,11 +690,13 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
     if (tid < G) { mypart[tid * PS] = m_s[tid]; mypart[tid * PS + 1] = l_s[tid]; }
   }
   __syncthreads();
+  HATA_CLK(8);
   if (tid == 0) {
     // release this partial (cumulative over bar.sync), acquire the others'
     const unsigned prev = atom_add_acq_rel_gpu(sync + 1, 1u);
     misc[2] = (prev == (unsigned)(M - 1));
   }
+  HATA_CLK(9);
   __syncthreads();
   HATA_TRACE(15);
   if (!misc[2]) return;
@@ -694,26 +707,38 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
     // rank rr's (m, l) and merge weight; every load below is independent
     const float* part = p.ws_part + (int64_t)u * M * PB;
     static_assert(D_HEAD % 32 == 0, "warp = one head");
-    for (int o = tid; o < G * D_HEAD; o += DEC_THREADS) {
-      const int h = o / D_HEAD, e = o % D_HEAD;
-      const float mr = lane < M ? __ldcg(part + lane * PB + h * PS) : -INFINITY;
-      const float lr = lane < M ? __ldcg(part + lane * PB + h * PS + 1) : 0.f;
-      float Mx = mr;
+    constexpr int NO = (GT * D_HEAD + DEC_THREADS - 1) / DEC_THREADS;   // outputs per thread
+    constexpr int OB = NO < 2 ? NO : 2;                                  // outputs per pass (registers)
+    for (int ob = 0; ob < NO; ob += OB) {
+      // issue every load of the pass before using any (one L2 round trip)
+      float mr[OB], lr[OB], v[OB][DEC_MAX_RANKS];
 #pragma unroll
-      for (int x = 16; x > 0; x >>= 1) Mx = fmaxf(Mx, __shfl_xor_sync(0xffffffffu, Mx, x));
-      const float w = (mr == -INFINITY) ? 0.f : expf(mr - Mx);
-      float Ls = lr * w;
+      for (int q = 0; q < OB; ++q) {
+        const int o = tid + (ob + q) * DEC_THREADS, h = o / D_HEAD, e = o % D_HEAD;
+        const bool ok = ob + q < NO && h < G;
+        mr[q] = ok && lane < M ? __ldcg(part + lane * PB + h * PS) : -INFINITY;
+        lr[q] = ok && lane < M ? __ldcg(part + lane * PB + h * PS + 1) : 0.f;
 #pragma unroll
-      for (int x = 16; x > 0; x >>= 1) Ls += __shfl_xor_sync(0xffffffffu, Ls, x);
-      float v[DEC_MAX_RANKS];                                        // every load in flight at once
+        for (int i = 0; i < DEC_MAX_RANKS; ++i) v[q][i] = ok && i < M ? __ldcg(part + i * PB + h * PS + 2 + e) : 0.f;
+      }
 #pragma unroll
-      for (int i = 0; i < DEC_MAX_RANKS; ++i) v[i] = i < M ? __ldcg(part + i * PB + h * PS + 2 + e) : 0.f;
-      float a0 = 0.f;
+      for (int q = 0; q < OB; ++q) {
+        const int o = tid + (ob + q) * DEC_THREADS, h = o / D_HEAD, e = o % D_HEAD;
+        float Mx = mr[q];
 #pragma unroll
-      for (int i = 0; i < DEC_MAX_RANKS; ++i) a0 = fmaf(v[i], __shfl_sync(0xffffffffu, w, i), a0);   // rank order
-      store_out(h, e, Ls > 0.f ? a0 / Ls : 0.f);
+        for (int x = 16; x > 0; x >>= 1) Mx = fmaxf(Mx, __shfl_xor_sync(0xffffffffu, Mx, x));
+        const float w = (mr[q] == -INFINITY) ? 0.f : expf(mr[q] - Mx);
+        float Ls = lr[q] * w;
+#pragma unroll
+        for (int x = 16; x > 0; x >>= 1) Ls += __shfl_xor_sync(0xffffffffu, Ls, x);
+        float a0 = 0.f;
+#pragma unroll
+        for (int i = 0; i < DEC_MAX_RANKS; ++i) a0 = fmaf(v[q][i], __shfl_sync(0xffffffffu, w, i), a0);   // rank order
+        if (ob + q < NO && h < G) store_out(h, e, Ls > 0.f ? a0 / Ls : 0.f);
+      }
     }
   }
+  HATA_CLK(10);
   // leave the workspace zeroed for the next launch (every rank has read the
   // unit total before publishing its partial)
   for (int i = tid; i <= p.nbins; i += DEC_THREADS) p.ws_tot[(int64_t)u * hs + i] = 0;

@@ -77,6 +77,14 @@ def main():
                 seg.append(f"{names[i]}={(b_[ok] - a_[ok]).median().item():.0f}")
         if seg:
             print(f"rep{rep} select cycles (t0 warp): " + " ".join(seg))
+        lastr = (t[:, 7] > 0) & (ck[:, 8] > 0) & (ck[:, 10] > 0)
+        if lastr.any():
+            c8, c9, c10, c14 = ck[lastr, 8], ck[lastr, 9], ck[lastr, 10], ck[lastr, 14]
+            print(f"rep{rep} combine cycles (last ranks): atomic={(c9 - c8).median().item():.0f} "
+                  f"merge={(c10 - c9).median().item():.0f} reset={(c14 - c10).median().item():.0f}")
+        nl = (t[:, 7] == 0) & (ck[:, 8] > 0) & (ck[:, 9] > 0)
+        if nl.any():
+            print(f"rep{rep} atomic cycles (other ranks): {(ck[nl, 9] - ck[nl, 8]).median().item():.0f}")
         for i in (8, 27, 5, 20, 15):
             c = t[:, i]
             if (c > 0).any():
