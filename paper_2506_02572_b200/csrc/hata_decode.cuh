@@ -144,7 +144,7 @@ __host__ __device__ inline DecodeSmem decode_smem_layout(const DecodeParams& p, 
   s.qf = off; off += up((GT + 1) * dec_qstride(p.d) * 4);
   s.qw = off; off += up((GT + 1) * (p.rbits / 32) * 4);
   s.qraw = off; off += up((GT + 2) * p.d * eb);   // q rows, new key, new value
-  s.planes = off; off += up(2 * 4 * 8 * 4);
+  s.planes = off; off += up((64 + 8) * 4);        // P/N planes [2][4][8] + K0 shares [8]
   s.rows = off; off += p.ws_rows ? 0 : up(p.R_cap * 4);
   s.red = off; off += up((DEC_MAX_RANKS * 4 + 64) * 4);
   s.chref = off; off += up(DEC_MAX_RANKS * 32);

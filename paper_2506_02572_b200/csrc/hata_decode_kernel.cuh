@@ -108,7 +108,7 @@ __device__ __forceinline__ void d_masks(const uint16_t* Dc, bool fromg, int j, i
 
 template <typename T, int W, int GT, int D_HEAD>
 __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __grid_constant__ DecodeParams p) {
-  constexpr int J = planes_for_group(GT);
+  constexpr int J = sw_planes_for_group(GT);                       // signed-weight planes
   constexpr int STAGE_TOK = DEC_STAGE_BYTES / (W * 4);
   constexpr int EB = sizeof(T);
   constexpr int NSL = AttnState<GT, D_HEAD>::NSL;
@@ -296,25 +296,38 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
     if (h < G && p.out_qcodes && r == 0) p.out_qcodes[((int64_t)b * p.Hq + g * G + h) * W + w] = word;
     if (h == G) const_cast<uint32_t*>(p.codes)[(int64_t)b * p.c_sb + (int64_t)g * p.c_sh + pos * W + w] = word;
   }
-  // bit planes of c_b = #{h: q_h bit b set} and of G - c_b (hata_score.cuh)
+  // signed-weight planes of w_b = G - 2 c_b, c_b = #{h: q_h bit b set}
+  // (hata_score.cuh): P_j / N_j and the constant K0, one warp per code word
+  const int sgn_s = (G % 2 == 0) ? 1 : 0;
   if (warp < W) {
     int c = 0;
     for (int h = 0; h < G; ++h) c += (qw[h * W + warp] >> lane) & 1u;
-    const int gc = G - c;
+    const int v = (G - 2 * c) >> sgn_s;                              // exact: G - 2c is even for even G
+    const int mag = v < 0 ? -v : v;
+    int negc = 0;
 #pragma unroll
     for (int j = 0; j < J; ++j) {
-      const uint32_t a = __ballot_sync(0xffffffffu, (c >> j) & 1);
-      const uint32_t bb = __ballot_sync(0xffffffffu, (gc >> j) & 1);
-      if (lane == 0) { planes[j * 8 + warp] = a; planes[32 + j * 8 + warp] = bb; }
+      const uint32_t pj = __ballot_sync(0xffffffffu, v > 0 && ((mag >> j) & 1));
+      const uint32_t nj = __ballot_sync(0xffffffffu, v < 0 && ((mag >> j) & 1));
+      negc += __popc(nj) << j;
+      if (lane == 0) { planes[j * 8 + warp] = pj; planes[32 + j * 8 + warp] = nj; }
     }
+    const int csum = warp_sum_i(c);
+    if (lane == 0) reinterpret_cast<int*>(planes)[64 + warp] = csum - (negc << sgn_s);   // K0 share of this word
   }
   HATA_TRACE(26);
   __syncthreads();
-  uint32_t A[J][W], Bp[J][W];
+  uint32_t A[J][W], Bp[J][W];                                       // P_j, N_j
 #pragma unroll
   for (int j = 0; j < J; ++j)
 #pragma unroll
     for (int w = 0; w < W; ++w) { A[j][w] = planes[j * 8 + w]; Bp[j][w] = planes[32 + j * 8 + w]; }
+  int K0 = 0;
+#pragma unroll
+  for (int w = 0; w < W; ++w) K0 += reinterpret_cast<const int*>(planes)[64 + w];
+  auto group_D = [&](const uint32_t (&kc)[W]) -> uint32_t {        // D = K0 + (T << s)
+    return (uint32_t)(K0 + (int)(group_distance_sw<W, J>(kc, A, Bp) << sgn_s));
+  };
 
   HATA_TRACE(1);
   // ---- phase 2: Hamming score + GQA sum (Alg. 3 lines 10-11) + histogram
@@ -355,10 +368,10 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
         smem_code(st, 2 * j2b, k2);
         smem_code(st, 2 * j2b + 1, k3);
       }
-      const uint32_t d0 = group_distance<W, J>(k0, A, Bp);
-      const uint32_t d1 = group_distance<W, J>(k1, A, Bp);
-      const uint32_t d2 = group_distance<W, J>(k2, A, Bp);
-      const uint32_t d3 = group_distance<W, J>(k3, A, Bp);
+      const uint32_t d0 = group_D(k0);
+      const uint32_t d1 = group_D(k1);
+      const uint32_t d2 = group_D(k2);
+      const uint32_t d3 = group_D(k3);
       atomicAdd(&hist[d0], 1u);
       atomicAdd(&hist[d1], 1u);
       if (p.d_smem) dsts[j2] = d0 | (d1 << 16);
@@ -382,7 +395,7 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
 #pragma unroll
         for (int w = 0; w < W; ++w) kc[w] = __ldg(gp + w);
       }
-      const uint32_t dv = group_distance<W, J>(kc, A, Bp);
+      const uint32_t dv = group_D(kc);
       atomicAdd(&hist[dv], 1u);
       Dloc[base + j] = (uint16_t)dv;
     }
@@ -399,7 +412,7 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
 #pragma unroll
     for (int w = 0; w < W; ++w) kc[w] = qw[G * W + w];
     const int jl = (int)(pos - t0);
-    const uint32_t Dn = group_distance<W, J>(kc, A, Bp);
+    const uint32_t Dn = group_D(kc);
     const uint32_t Do = Dloc[jl];
     hist[Do] -= 1u;
     hist[Dn] += 1u;

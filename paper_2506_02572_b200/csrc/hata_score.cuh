@@ -85,4 +85,64 @@ __device__ __forceinline__ uint32_t group_distance(const uint32_t (&k)[W], const
   }
 }
 
+// ---------------------------------------------------------------------------
+// Signed-weight form (fewer weighted words than the (c, G - c) planes above).
+// With w_b = G - 2 c_b:  D(k) = C0 + sum_b k_b w_b,  C0 = sum_b c_b.
+// For even G every w_b is even: v_b = w_b >> s (s = 1 for even G, else 0).
+// Split v_b by sign into magnitude planes P_j (v_b > 0, bit j of |v_b|) and
+// N_j (v_b < 0, bit j of |v_b|).  Since popc(k & N) = popc(N) - popc(~k & N)
+// and P_j, N_j are disjoint:
+//   D(k) = K0 + 2^s * sum_j 2^j popc((k & P_j) | (~k & N_j)),
+//   K0   = C0 - 2^s * sum_j 2^j popc(N_j),
+// one LOP3 per (plane, word).  Planes per group template: |v| <= G/2 (even G)
+// or G (odd G) over the G the template serves.
+constexpr __host__ __device__ int sw_planes_for_group(int GT) {
+  return GT <= 2 ? 1 : (GT <= 4 ? 2 : 3);
+}
+
+__device__ __forceinline__ uint32_t lop_sel(uint32_t k, uint32_t P, uint32_t N) {   // (k & P) | (~k & N)
+  return lop_mux(k, P, N);
+}
+
+// T = sum_j 2^j popc(M_j) over the W words (D = K0 + (T << s)).
+template <int W, int JP>
+__device__ __forceinline__ uint32_t group_distance_sw(const uint32_t (&k)[W], const uint32_t (&P)[JP][W],
+                                                      const uint32_t (&N)[JP][W]) {
+  uint32_t m[JP][W];
+#pragma unroll
+  for (int j = 0; j < JP; ++j)
+#pragma unroll
+    for (int w = 0; w < W; ++w) m[j][w] = lop_sel(k[w], P[j][w], N[j][w]);
+  if constexpr (W == 4 && JP == 2) {
+    uint32_t s0, c0, s1, c1, l1, c2, l2, l3;
+    full_add(m[0][0], m[0][1], m[0][2], s0, c0);
+    const uint32_t l0 = s0 ^ m[0][3], c0b = s0 & m[0][3];        // weight 1 | carries weight 2
+    full_add(m[1][0], m[1][1], m[1][2], s1, c1);
+    const uint32_t t = s1 ^ m[1][3], c1b = s1 & m[1][3];         // weight 2 | carries weight 4
+    full_add(c0, c0b, t, l1, c2);                                // weight 2 | weight 4
+    full_add(c1, c1b, c2, l2, l3);                               // weight 4 | weight 8
+    return __popc(l0) + 2u * __popc(l1) + 4u * __popc(l2) + 8u * __popc(l3);
+  } else if constexpr (W == 4 && JP == 3) {
+    uint32_t s0, c0;
+    full_add(m[0][0], m[0][1], m[0][2], s0, c0);
+    uint32_t l0 = s0 ^ m[0][3], c0b = s0 & m[0][3];
+    uint32_t s1, c1, s1b, c1b;
+    full_add(m[1][0], m[1][1], m[1][2], s1, c1);
+    full_add(m[1][3], c0, c0b, s1b, c1b);
+    uint32_t l1 = s1 ^ s1b, c1c = s1 & s1b;
+    uint32_t s2, c2, s2b, c2b, l2, c2c;
+    full_add(m[2][0], m[2][1], m[2][2], s2, c2);
+    full_add(m[2][3], c1, c1b, s2b, c2b);
+    full_add(s2, s2b, c1c, l2, c2c);
+    uint32_t l3, l4;
+    full_add(c2, c2b, c2c, l3, l4);
+    return __popc(l0) + 2u * __popc(l1) + 4u * __popc(l2) + 8u * __popc(l3) + 16u * __popc(l4);
+  } else {
+    uint32_t d = 0;
+#pragma unroll
+    for (int j = 0; j < JP; ++j) d += popc_words<W>(m[j]) << j;
+    return d;
+  }
+}
+
 }  // namespace hata
