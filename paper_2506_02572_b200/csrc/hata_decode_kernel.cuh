@@ -619,17 +619,19 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
         }
         const uint32_t sel8 = lt8 | tie8;
         const int base = lt_b + min(ti_b, quota);                    // position of the block's first pick
-        const uint32_t wv[4] = {x.x, x.y, x.z, x.w};
-        for (uint32_t m = sel8; m; m &= m - 1u) {
-          const int i = __ffs(m) - 1;
-          const int pl = base + __popc(sel8 & ((1u << i) - 1u));
-          const int tok = (tid * S8 + c) * 8 + i;
-          rows[pl] = (int32_t)t0 + tok;
-          const int pos = off0 + pl;
-          if (oidx) oidx[pos] = (int32_t)(t0 + tok + p.token_offset);
-          const int dv = (int)((wv[i >> 1] >> (16 * (i & 1))) & 0xffffu);
-          if (osc) osc[pos] = Gr - 2 * dv;                           // S = G*rbits - 2D
-          if (ocd) ocd[pos] = dv;
+        // only the rows list is on the critical path; out_idx / out_score /
+        // cand_D are written from it after the attention (coalesced)
+        auto emit = [&](int pl, int i) { rows[pl] = (int32_t)t0 + (tid * S8 + c) * 8 + i; };
+        if (__popc(sel8) >= 3) {                                     // dense block (e.g. a recent window):
+          int rr = 0;                                                // predicated, no per-pick popc
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            if ((sel8 >> i) & 1u) emit(base + rr++, i);
+        } else {
+          for (uint32_t m = sel8; m; m &= m - 1u) {
+            const int i = __ffs(m) - 1;
+            emit(base + __popc(sel8 & ((1u << i) - 1u)), i);
+          }
         }
         lt_b += __popc(lt8);
         ti_b += __popc(eq8);
@@ -666,6 +668,17 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
     }
   }
   HATA_TRACE(6);
+  // optional outputs of the selection (Alg. 3 line 13): this rank's rows are
+  // positions [off0, off0 + Rr) of the ascending k'-list
+  if (oidx || osc || ocd) {
+    for (int i = tid; i < Rr; i += DEC_THREADS) {
+      const int32_t row = rows[i];
+      const int dv = (int)Dloc[row - (int32_t)t0];
+      if (oidx) oidx[off0 + i] = (int32_t)(row + p.token_offset);
+      if (osc) osc[off0 + i] = Gr - 2 * dv;                          // S = G*rbits - 2D
+      if (ocd) ocd[off0 + i] = dv;
+    }
+  }
 
   // ---- phase 5: merge the M rank partials in rank order (flash-decoding combine)
   const int64_t orow = (int64_t)b * p.Hq + (int64_t)g * G;      // first output row of the group
