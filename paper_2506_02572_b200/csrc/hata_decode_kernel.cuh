@@ -221,18 +221,25 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
     // 5-7) straight from the accumulator fragment via ballots.
     const int gid = lane >> 2, tig = lane & 3;
     uint8_t* qbytes = reinterpret_cast<uint8_t*>(qw);               // [GT+1][W*4] code bytes
+    // A fragments of every k-step, read once from the bf16 rows as stored
+    constexpr int KS = D_HEAD / 16;
+    uint32_t qa[KS][4];
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) {
+      const uint32_t* x0 = reinterpret_cast<const uint32_t*>(qraw + gid * D_HEAD + ks * 16 + 2 * tig);
+      const uint32_t* x1 = reinterpret_cast<const uint32_t*>(qraw + (gid + 8) * D_HEAD + ks * 16 + 2 * tig);
+      qa[ks][0] = gid < NV ? x0[0] : 0u;
+      qa[ks][1] = gid + 8 < NV ? x1[0] : 0u;
+      qa[ks][2] = gid < NV ? x0[4] : 0u;
+      qa[ks][3] = gid + 8 < NV ? x1[4] : 0u;
+    }
     for (int nt = warp; nt < p.rbits / 8; nt += DEC_WARPS) {
       float c[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-      for (int k0 = 0; k0 < D_HEAD; k0 += 16) {
-        // A fragment straight from the bf16 rows as stored (adjacent pairs)
-        const uint32_t* x0 = reinterpret_cast<const uint32_t*>(qraw + gid * D_HEAD + k0 + 2 * tig);
-        const uint32_t* x1 = reinterpret_cast<const uint32_t*>(qraw + (gid + 8) * D_HEAD + k0 + 2 * tig);
-        const uint32_t a[4] = {gid < NV ? x0[0] : 0u, gid + 8 < NV ? x1[0] : 0u, gid < NV ? x0[4] : 0u,
-                               gid + 8 < NV ? x1[4] : 0u};
+      for (int ks = 0; ks < KS; ++ks) {
         uint32_t b0, b1;
-        ldsm_x2_trans(b0, b1, reinterpret_cast<const uint8_t*>(Ws) + (k0 + (lane & 15)) * WROWB + nt * 16);
-        mma_bf16_16816(c, a, b0, b1);
+        ldsm_x2_trans(b0, b1, reinterpret_cast<const uint8_t*>(Ws) + (ks * 16 + (lane & 15)) * WROWB + nt * 16);
+        mma_bf16_16816(c, qa[ks], b0, b1);
       }
       const uint32_t m0 = __ballot_sync(0xffffffffu, c[0] >= 0.f), m1 = __ballot_sync(0xffffffffu, c[1] >= 0.f);
       const uint32_t m2 = __ballot_sync(0xffffffffu, c[2] >= 0.f), m3 = __ballot_sync(0xffffffffu, c[3] >= 0.f);
@@ -346,7 +353,7 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
   int slot = 0;
   uint32_t parity = 0;
   for (int s = 0; s < nstages; ++s) {
-    mbar_wait(&bars[slot], parity);
+    if (!(HATA_DIAG && (p.dbg & 16))) mbar_wait(&bars[slot], parity);   // dbg 16: timing without waiting for the stream
     if (s == 0) HATA_TRACE(10);
     if (s == nstages - 1) HATA_TRACE(13);
     const int base = s * STAGE_TOK;
@@ -372,13 +379,13 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
       const uint32_t d1 = group_D(k1);
       const uint32_t d2 = group_D(k2);
       const uint32_t d3 = group_D(k3);
-      atomicAdd(&hist[d0], 1u);
-      atomicAdd(&hist[d1], 1u);
+      if (!(HATA_DIAG && (p.dbg & 2))) atomicAdd(&hist[d0], 1u);   // dbg 2: timing without the histogram
+      if (!(HATA_DIAG && (p.dbg & 2))) atomicAdd(&hist[d1], 1u);   // dbg 2: timing without the histogram
       if (p.d_smem) dsts[j2] = d0 | (d1 << 16);
       else dst[j2] = d0 | (d1 << 16);
       if (two) {
-        atomicAdd(&hist[d2], 1u);
-        atomicAdd(&hist[d3], 1u);
+        if (!(HATA_DIAG && (p.dbg & 2))) atomicAdd(&hist[d2], 1u);   // dbg 2: timing without the histogram
+        if (!(HATA_DIAG && (p.dbg & 2))) atomicAdd(&hist[d3], 1u);   // dbg 2: timing without the histogram
         if (p.d_smem) dsts[j2b] = d2 | (d3 << 16);
         else dst[j2b] = d2 | (d3 << 16);
       }
@@ -726,48 +733,60 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
   __syncthreads();
   HATA_TRACE(15);
   if (!misc[2]) return;
+  // leave the workspace zeroed for the next launch: every rank read the unit
+  // total before publishing its partial (stores overlap the merge loads)
+  for (int i = tid; i <= p.nbins; i += DEC_THREADS) p.ws_tot[(int64_t)u * hs + i] = 0;
   // last rank: every partial is visible (writer fence + counter); merge them
   // in rank order straight from L2 (thread = one output element)
   if (!p.cand_mode) {
-    // a warp's 32 outputs share the head h (D_HEAD % 32 == 0): lane rr holds
-    // rank rr's (m, l) and merge weight; every load below is independent
+    // merge weights once per head: warp h (< G) holds rank r in lane r,
+    // w[r][h] = e^{m_r - M_h} and 1 / L_h go to smem; every output thread
+    // issues its M partial loads up front (one L2 round trip)
     const float* part = p.ws_part + (int64_t)u * M * PB;
-    static_assert(D_HEAD % 32 == 0, "warp = one head");
+    float* wts = reinterpret_cast<float*>(smem + L.ring);             // [DEC_MAX_RANKS][GT] + [GT] (ring is free)
+    float* linv = wts + DEC_MAX_RANKS * GT;
     constexpr int NO = (GT * D_HEAD + DEC_THREADS - 1) / DEC_THREADS;   // outputs per thread
     constexpr int OB = NO < 2 ? NO : 2;                                  // outputs per pass (registers)
-    for (int ob = 0; ob < NO; ob += OB) {
-      // issue every load of the pass before using any (one L2 round trip)
-      float mr[OB], lr[OB], v[OB][DEC_MAX_RANKS];
+    float v[OB][DEC_MAX_RANKS];
+    auto load_pass = [&](int ob) {
 #pragma unroll
       for (int q = 0; q < OB; ++q) {
         const int o = tid + (ob + q) * DEC_THREADS, h = o / D_HEAD, e = o % D_HEAD;
         const bool ok = ob + q < NO && h < G;
-        mr[q] = ok && lane < M ? __ldcg(part + lane * PB + h * PS) : -INFINITY;
-        lr[q] = ok && lane < M ? __ldcg(part + lane * PB + h * PS + 1) : 0.f;
 #pragma unroll
         for (int i = 0; i < DEC_MAX_RANKS; ++i) v[q][i] = ok && i < M ? __ldcg(part + i * PB + h * PS + 2 + e) : 0.f;
       }
+    };
+    load_pass(0);
+    if (warp < G) {
+      const float mr = lane < M ? __ldcg(part + lane * PB + warp * PS) : -INFINITY;
+      const float lr = lane < M ? __ldcg(part + lane * PB + warp * PS + 1) : 0.f;
+      float Mx = mr;
+#pragma unroll
+      for (int x = 16; x > 0; x >>= 1) Mx = fmaxf(Mx, __shfl_xor_sync(0xffffffffu, Mx, x));
+      const float w = (mr == -INFINITY) ? 0.f : expf(mr - Mx);
+      float Ls = lr * w;
+#pragma unroll
+      for (int x = 16; x > 0; x >>= 1) Ls += __shfl_xor_sync(0xffffffffu, Ls, x);
+      if (lane < DEC_MAX_RANKS) wts[lane * GT + warp] = w;
+      if (lane == 0) linv[warp] = Ls > 0.f ? 1.f / Ls : 0.f;
+    }
+    __syncthreads();
+    for (int ob = 0; ob < NO; ob += OB) {
+      if (ob) load_pass(ob);
 #pragma unroll
       for (int q = 0; q < OB; ++q) {
         const int o = tid + (ob + q) * DEC_THREADS, h = o / D_HEAD, e = o % D_HEAD;
-        float Mx = mr[q];
+        if (ob + q < NO && h < G) {
+          float a0 = 0.f;
 #pragma unroll
-        for (int x = 16; x > 0; x >>= 1) Mx = fmaxf(Mx, __shfl_xor_sync(0xffffffffu, Mx, x));
-        const float w = (mr[q] == -INFINITY) ? 0.f : expf(mr[q] - Mx);
-        float Ls = lr[q] * w;
-#pragma unroll
-        for (int x = 16; x > 0; x >>= 1) Ls += __shfl_xor_sync(0xffffffffu, Ls, x);
-        float a0 = 0.f;
-#pragma unroll
-        for (int i = 0; i < DEC_MAX_RANKS; ++i) a0 = fmaf(v[q][i], __shfl_sync(0xffffffffu, w, i), a0);   // rank order
-        if (ob + q < NO && h < G) store_out(h, e, Ls > 0.f ? a0 / Ls : 0.f);
+          for (int i = 0; i < DEC_MAX_RANKS; ++i) a0 = fmaf(v[q][i], wts[i * GT + h], a0);   // rank order
+          store_out(h, e, a0 * linv[h]);
+        }
       }
     }
   }
   HATA_CLK(10);
-  // leave the workspace zeroed for the next launch (every rank has read the
-  // unit total before publishing its partial)
-  for (int i = tid; i <= p.nbins; i += DEC_THREADS) p.ws_tot[(int64_t)u * hs + i] = 0;
   if (tid == 0) { sync[0] = 0u; sync[1] = 0u; }
   HATA_TRACE(7);
   HATA_CLK(14);

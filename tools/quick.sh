@@ -1,6 +1,6 @@
 #!/bin/bash
 # quick GPU check: parity subset + trace + bench (+ optional HATA_DEBUG variants in $DBGS)
-timeout 900 python -m pytest tests/ -q -m gpu -x -k "not full_size_batched and not shard" 2>&1 | tail -1 | sed "s/^/pytest: /"
+timeout 900 python -m pytest tests/ -q -m gpu -x -k "not full_size_batched and not shard" 2>&1 | grep -E "passed|failed|error" | sed "s/^/pytest: /"
 python tools/trace_decode.py cfg4 3 1 2>&1 | tail -2
 for d in 0 $DBGS; do
   echo -n "dbg=$d bench: "
