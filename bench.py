@@ -234,6 +234,29 @@ def bench_e2e(sh, steps, device):
                 h2d_bytes_per_step=h2d, d2h_bytes_per_step=d2h)
 
 
+def bench_hash_keys(st, reps):
+    """Prefill key hash (hata_hash_keys, §8(a) a1) over the whole cache of one step:
+    B*H_kv*N*d bf16 keys -> codes, tensor cores.  Reported separately (off the
+    per-token decode path)."""
+    sh = st.sh
+    n = sh.N - 1
+    st.H.hash_keys(st.K, st.W, st.codes, 0, n)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        st.H.hash_keys(st.K, st.W, st.codes, 0, n)
+    e1.record()
+    e1.synchronize()
+    us = e0.elapsed_time(e1) / reps * 1e3
+    eb = 2 if sh.dtype == "bf16" else 4
+    kbytes = sh.B * sh.Hkv * n * sh.d * eb
+    flops = 2.0 * sh.B * sh.Hkv * n * sh.d * sh.rbits
+    return {"us": us, "keys": sh.B * sh.Hkv * n, "GBps_K_read": kbytes / (us * 1e-6) / 1e9,
+            "TFLOPs": flops / (us * 1e-6) / 1e12, "kernel": "hash_keys_mma_kernel (mma.sync bf16, fp32 acc)",
+            "note": "cache resident from the previous call (L2 holds at most 126 MB of the K read)"}
+
+
 def dense_baseline(st, steps):
     """Full-attention decode over the same cache (context, north_star)."""
     q = st.q.view(st.sh.B, st.sh.Hq, 1, st.sh.d)
@@ -526,6 +549,7 @@ def main():
             del r2
         line["secondary"] = sec
     st = Step(sh, 1000, device)
+    line["hash_keys"] = bench_hash_keys(st, 20)
     line["dense_baseline"] = dense_baseline(st, 50)
     line["dense_baseline"]["speedup_vs_dense"] = line["dense_baseline"]["us_per_step"] / us_dec
     del st

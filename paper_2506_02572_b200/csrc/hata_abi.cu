@@ -108,7 +108,8 @@ hata_status hata_hash_keys(const void* K, hata_strides ks, hata_dtype dt, const 
       !dtype_ok(dt))
     return HATA_ERR_INVALID_ARG;
   if (!shape_supported(d, rbits, 1)) return HATA_ERR_UNSUPPORTED;
-  if (!kv_layout_ok(K, ks, elem_bytes(dt), d) || cs.st != rbits / 32 || !aligned(codes, 4)) return HATA_ERR_INVALID_ARG;
+  if (!kv_layout_ok(K, ks, elem_bytes(dt), d) || cs.st != rbits / 32 || !aligned(codes, 4) || !aligned(W, 16))
+    return HATA_ERR_INVALID_ARG;
   if (n == 0) return HATA_OK;
   hata::HashKeysParams p = {};
   p.K = K; p.kv_sb = ks.sb; p.kv_sh = ks.sh; p.kv_st = ks.st;

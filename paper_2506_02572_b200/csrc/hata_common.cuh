@@ -61,6 +61,10 @@ __device__ __forceinline__ void load_row_slice(const T* __restrict__ p, float (&
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
+// 16-byte cp.async global -> shared (L2-only caching)
+__device__ __forceinline__ void cp_async16_g(void* smem_dst, const void* gsrc) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem_dst)), "l"(gsrc) : "memory");
+}
 __device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t cnt) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(cnt));
 }

@@ -1,5 +1,160 @@
-// tcgen05 (UMMA) key-hash GEMM: placeholder until the tensor-core path lands.
+// Prefill key hash on the tensor cores (bf16): codes = pack(sign(K_tile . W_g)).
+//
+// PAPER: Alg. 1 lines 2-5 with HashEncode = Alg. 2:
+// Sign(MatMul(K, W_H)) -> BitPack, done once per cached key at prefill
+// ("<1% of total computation").
+//
+// A K tile = 128 tokens of one (b, g) x all rbits output bits; 8 warps, warp
+// w owns tokens [16w, 16w+16).  K tiles and W_g are staged in smem (padded rows, so
+// the ldmatrix fragments are bank-conflict free); every 16 x 8 output tile is
+// one chain of D/16 mma.sync m16n8k16 (bf16 products are exact, fp32
+// accumulation, R13); the sign bits are packed straight from the accumulator
+// fragments by ballots into LSB-first uint32 words (R6, R7).
+//
+// This is the legacy-MMA (HMMA) path: at rbits = 128 the projection needs
+// 128 flop per K byte, so HMMA (~0.58 PFLOP/s on this part) rather than HBM
+// bounds it; a tcgen05/TMEM version is the next step.
 #include "hata_internal.h"
+#include "hata_common.cuh"
+
 namespace hata {
-cudaError_t launch_hash_keys_tc(const HashKeysParams&, cudaStream_t) { return cudaErrorNotSupported; }
+
+constexpr int HK_TOK = 128;                  // tokens per CTA
+constexpr int HK_THREADS = 256;
+
+// Persistent CTAs: CTA (x, u) hashes token tiles x, x + nx, x + 2 nx, ... of
+// unit u = (b, g); W_g is staged once, K tiles are double-buffered with
+// cp.async (the next tile streams in while the current one is on the MMAs).
+template <int RB>                             // rbits
+__global__ void __launch_bounds__(HK_THREADS) hash_keys_mma_kernel(const HashKeysParams p) {
+  constexpr int D = 128;
+  constexpr int W = RB / 32;
+  constexpr int XROW = D * 2 + 16;            // padded smem row of the K tile (bytes)
+  constexpr int WROW = RB * 2 + 16;           // padded smem row of W_g (bytes)
+  extern __shared__ __align__(128) uint8_t sm[];
+  uint8_t* ws = sm;                           // [D][WROW]
+  uint8_t* xs0 = sm + D * WROW;               // 2 x [HK_TOK][XROW]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int gid = lane >> 2, tig = lane & 3;
+  const int bg = blockIdx.y, b = bg / p.Hkv, g = bg % p.Hkv;
+  const int ntiles = (int)((p.n + HK_TOK - 1) / HK_TOK);
+  const __nv_bfloat16* Kb = reinterpret_cast<const __nv_bfloat16*>(p.K) + (int64_t)b * p.kv_sb + (int64_t)g * p.kv_sh;
+  const __nv_bfloat16* Wg = reinterpret_cast<const __nv_bfloat16*>(p.Wh) + (int64_t)g * D * RB;
+  uint32_t* cb = p.codes + (int64_t)b * p.c_sb + (int64_t)g * p.c_sh;
+  constexpr int XCH = D * 2 / 16, WCH = RB * 2 / 16;
+
+  auto stage_k = [&](int tile, uint8_t* xs) {   // K rows past the end are zero
+    const int64_t tbase = p.t0 + (int64_t)tile * HK_TOK;
+    const int ntok = (int)min((int64_t)HK_TOK, p.t0 + p.n - tbase);
+    for (int i = tid; i < HK_TOK * XCH; i += HK_THREADS) {
+      const int r = i / XCH, c = i % XCH;
+      uint8_t* dst = xs + r * XROW + c * 16;
+      if (r < ntok) cp_async16_g(dst, reinterpret_cast<const uint4*>(Kb + (tbase + r) * p.kv_st) + c);
+      else *reinterpret_cast<uint4*>(dst) = make_uint4(0, 0, 0, 0);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  for (int i = tid; i < D * WCH; i += HK_THREADS) {
+    const int r = i / WCH, c = i % WCH;
+    *reinterpret_cast<uint4*>(ws + r * WROW + c * 16) = __ldg(reinterpret_cast<const uint4*>(Wg + (int64_t)r * RB) + c);
+  }
+  int buf = 0;
+  if ((int)blockIdx.x < ntiles) stage_k(blockIdx.x, xs0);
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int next = tile + gridDim.x;
+    uint8_t* xs = xs0 + buf * (HK_TOK * XROW);
+    if (next < ntiles) {
+      stage_k(next, xs0 + (buf ^ 1) * (HK_TOK * XROW));
+      asm volatile("cp.async.wait_group 1;" ::: "memory");       // current tile landed
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
+    __syncthreads();
+
+    constexpr int KS = D / 16;
+    uint32_t a[KS][4];
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) {
+      const uint8_t* ap = xs + (warp * 16 + (lane & 15)) * XROW + ks * 32 + (lane >> 4) * 16;
+      asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0, %1, %2, %3}, [%4];"
+                   : "=r"(a[ks][0]), "=r"(a[ks][1]), "=r"(a[ks][2]), "=r"(a[ks][3])
+                   : "r"(smem_u32(ap)));
+    }
+    uint32_t wlo[W], whi[W];                  // code words of rows gid and gid + 8
+#pragma unroll
+    for (int w = 0; w < W; ++w) wlo[w] = whi[w] = 0u;
+#pragma unroll
+    for (int nt0 = 0; nt0 < RB / 8; nt0 += 2) {   // two independent accumulator chains
+      float c[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+#pragma unroll
+      for (int ks = 0; ks < KS; ++ks)
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          uint32_t b0, b1;
+          ldsm_x2_trans(b0, b1, ws + (ks * 16 + (lane & 15)) * WROW + (nt0 + q) * 16);
+          mma_bf16_16816(c[q], a[ks], b0, b1);
+        }
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int nt = nt0 + q;
+        // c0, c1: row gid, bits nt*8 + 2 tig (+1); c2, c3: row gid + 8
+        const uint32_t m0 = __ballot_sync(0xffffffffu, c[q][0] >= 0.f), m1 = __ballot_sync(0xffffffffu, c[q][1] >= 0.f);
+        const uint32_t m2 = __ballot_sync(0xffffffffu, c[q][2] >= 0.f), m3 = __ballot_sync(0xffffffffu, c[q][3] >= 0.f);
+        uint32_t lo = 0, hi = 0;              // bits nt*8 .. nt*8+7 of rows gid / gid+8, LSB-first (R7)
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          lo |= ((m0 >> (gid * 4 + t)) & 1u) << (2 * t) | ((m1 >> (gid * 4 + t)) & 1u) << (2 * t + 1);
+          hi |= ((m2 >> (gid * 4 + t)) & 1u) << (2 * t) | ((m3 >> (gid * 4 + t)) & 1u) << (2 * t + 1);
+        }
+        wlo[nt / 4] |= lo << (8 * (nt % 4));
+        whi[nt / 4] |= hi << (8 * (nt % 4));
+      }
+    }
+    if (tig == 0) {
+      const int64_t tbase = p.t0 + (int64_t)tile * HK_TOK;
+      const int ntok = (int)min((int64_t)HK_TOK, p.t0 + p.n - tbase);
+      const int r0 = warp * 16 + gid, r1 = r0 + 8;
+      if (r0 < ntok) {
+#pragma unroll
+        for (int w = 0; w < W; ++w) cb[(tbase + r0) * W + w] = wlo[w];
+      }
+      if (r1 < ntok) {
+#pragma unroll
+        for (int w = 0; w < W; ++w) cb[(tbase + r1) * W + w] = whi[w];
+      }
+    }
+    __syncthreads();                          // this buffer is refilled two tiles on
+    buf ^= 1;
+  }
+}
+
+template <int RB>
+static cudaError_t launch_rb(const HashKeysParams& p, cudaStream_t s) {
+  const size_t smem = (size_t)128 * (RB * 2 + 16) + 2 * (size_t)HK_TOK * (128 * 2 + 16);
+  cudaError_t e = cudaFuncSetAttribute(hash_keys_mma_kernel<RB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  const int units = p.B * p.Hkv;
+  const int ntiles = (int)((p.n + HK_TOK - 1) / HK_TOK);
+  int per_sm = (int)(227 * 1024 / smem);
+  if (per_sm < 1) per_sm = 1;
+  int nx = (device_sm_count() * per_sm + units - 1) / units;   // CTAs per unit: fill the chip once
+  if (nx > ntiles) nx = ntiles;
+  if (nx < 1) nx = 1;
+  hash_keys_mma_kernel<RB><<<dim3(nx, units), HK_THREADS, smem, s>>>(p);
+  return cudaGetLastError();
+}
+
+// bf16, d = 128: rbits in {32, 64, 128, 256}; anything else -> not supported
+// (the caller falls back to the CUDA-core kernel).
+cudaError_t launch_hash_keys_tc(const HashKeysParams& p, cudaStream_t s) {
+  if (p.d != 128 || p.n <= 0) return p.n <= 0 ? cudaSuccess : cudaErrorNotSupported;
+  switch (p.rbits) {
+    case 32: return launch_rb<32>(p, s);
+    case 64: return launch_rb<64>(p, s);
+    case 128: return launch_rb<128>(p, s);
+    case 256: return launch_rb<256>(p, s);
+  }
+  return cudaErrorNotSupported;
+}
+
 }  // namespace hata
