@@ -17,12 +17,17 @@ INCLUDE = os.path.join(ROOT, "include")
 # HATA_TRACE_BUILD=1: the diagnostics variant (phase stamps compiled in) for
 # tools/trace_decode.py -> libhata_trace.so; the product is libhata.so
 TRACE = os.environ.get("HATA_TRACE_BUILD") == "1"
-OUT = os.path.join(HERE, "libhata_trace.so" if TRACE else "libhata.so")
-OBJ = os.path.join(HERE, "_build_trace" if TRACE else "_build")
+# HATA_VARIANT=name HATA_DEFS="-DX=1 ...": an experimental build libhata_<name>.so
+# (selected at run time with HATA_LIB); never the product
+VARIANT = os.environ.get("HATA_VARIANT", "")
+DEFS = os.environ.get("HATA_DEFS", "").split() if VARIANT else []
+_name = "libhata" + ("_trace" if TRACE else "") + ("_" + VARIANT if VARIANT else "")
+OUT = os.path.join(HERE, _name + ".so")
+OBJ = os.path.join(HERE, "_build" + ("_trace" if TRACE else "") + ("_" + VARIANT if VARIANT else ""))
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
-         "-Xptxas", "-v", "-I", INCLUDE, "-I", CSRC] + (["-DHATA_TRACE_ENABLED=1"] if TRACE else [])
+         "-Xptxas", "-v", "-I", INCLUDE, "-I", CSRC] + (["-DHATA_TRACE_ENABLED=1"] if TRACE else []) + DEFS
 SOURCES = ["hata_abi.cu", "hata_decode.cu", "hata_hash.cu", "hata_hash_tc.cu", "hata_shard.cu"]
 
 

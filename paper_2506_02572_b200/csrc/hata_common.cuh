@@ -97,6 +97,11 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
+// Programmatic dependent launch (griddepcontrol): wait for the preceding
+// grid's completion + memory flush; allow the dependent grid to launch.
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // Bitwise select: k ? b : a  (one LOP3).
 __device__ __forceinline__ uint32_t lop_mux(uint32_t k, uint32_t b, uint32_t a) {
   uint32_t r;

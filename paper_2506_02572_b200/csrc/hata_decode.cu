@@ -146,7 +146,7 @@ cudaError_t launch_decode(DecodeParams& p, const DecodePlan& pl, void* ws, int i
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, pl.smem);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
-  cudaLaunchAttribute at[1];
+  cudaLaunchAttribute at[2];
   cfg.gridDim = dim3(pl.M, p.B * p.Hkv);
   cfg.blockDim = dim3(DEC_THREADS);
   cfg.dynamicSmemBytes = pl.smem;
@@ -156,6 +156,15 @@ cudaError_t launch_decode(DecodeParams& p, const DecodePlan& pl, void* ws, int i
   at[0].val.cooperative = (pl.M > 1 && !(p.dbg & 8)) ? 1 : 0;
   cfg.attrs = at;
   cfg.numAttrs = 1;
+  // programmatic dependent launch: the prologue (barrier init, W_g loads)
+  // overlaps the tail of the preceding kernel in the stream; the kernel waits
+  // (griddepcontrol.wait) before touching anything that kernel may produce
+  static const int pdl = [] { const char* e = std::getenv("HATA_PDL"); return e ? std::atoi(e) : 1; }();
+  if (pdl) {
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.numAttrs = 2;
+  }
   return cudaLaunchKernelEx(&cfg, kern, (const DecodeParams)p);
 }
 

@@ -20,7 +20,10 @@
 
 namespace hata {
 
-constexpr int DEC_THREADS = 256;
+#ifndef HATA_DEC_THREADS
+#define HATA_DEC_THREADS 256
+#endif
+constexpr int DEC_THREADS = HATA_DEC_THREADS;
 constexpr int DEC_WARPS = DEC_THREADS / 32;
 constexpr int DEC_STAGE_BYTES = 32768;       // one bulk copy of codes (few large TMA requests)
 constexpr int DEC_MAX_STAGES = 4;            // code ring depth (up to 128 KB in flight)
@@ -29,6 +32,10 @@ constexpr int DEC_CHUNK_ALIGN = 64;          // tokens
 constexpr int DEC_MAX_RANKS = 32;            // M cap (histogram exchange is M x nbins per rank)
 constexpr int DEC_ROW_PAD = 16;              // bytes of padding per staged K/V row (bank spread)
 constexpr int DEC_QS_PAD = 4;                // floats of padding per q row in smem
+// spin-wait rounds before a kernel traps instead of hanging (~seconds)
+#ifndef HATA_SPIN_LIMIT
+#define HATA_SPIN_LIMIT (1u << 24)
+#endif
 
 struct DecodeParams {
   const void* q;           // [B, Hq, d] contiguous

@@ -116,6 +116,9 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
   HATA_TRACE(31);
   HATA_CLK(23);
   if (HATA_DIAG && (p.dbg & 4)) return;                            // diagnostics: launch cost only
+  // a dependent launch may start its prologue (W_g loads) on SMs this grid
+  // frees; it waits for this grid's completion before reading anything else
+  griddep_launch_dependents();
 
   const int M = p.M;
   const int NST = p.stages;
@@ -165,21 +168,14 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
     mbar_arrive_expect_tx(&bars[slot], bytes);
     if (bytes) bulk_g2s(ring + slot * DEC_STAGE_BYTES, cbase + (t0 + (int64_t)s * STAGE_TOK) * W, bytes, &bars[slot]);
   };
-  const int64_t n = p.n[b];                                         // requested before the streams
   const int WROWB = dec_wrow_stride(p.rbits, EB);                   // padded smem row of W_g
   const uint32_t wrow = (uint32_t)(p.rbits * EB);                  // bytes of one W_g row
   if (tid == 0) {
-    // [0, NST) code ring, NST: W_g + q + k_new, NST+1: spare, NST+2: spare,
+    // [0, NST) code ring, NST: W_g, NST+1: q + k_new + v_new, NST+2: spare,
     // NST+3: attention gather batches
     for (int s = 0; s < NST + 4; ++s) mbar_init(&bars[s], 1);
     fence_mbar_init();
-    const uint32_t qbytes = (uint32_t)(G * D_HEAD * EB), kbytes = append ? (uint32_t)(D_HEAD * EB) : 0u;
-    mbar_arrive_expect_tx(&bars[NST], D_HEAD * wrow + qbytes + 2 * kbytes);
-    bulk_g2s(qraw, qg, qbytes, &bars[NST]);
-    if (kbytes) {                                                   // new key and value rows
-      bulk_g2s(qraw + G * D_HEAD, reinterpret_cast<const T*>(p.k_new) + (int64_t)u * D_HEAD, kbytes, &bars[NST]);
-      bulk_g2s(qraw + (G + 1) * D_HEAD, reinterpret_cast<const T*>(p.v_new) + (int64_t)u * D_HEAD, kbytes, &bars[NST]);
-    }
+    mbar_arrive_expect_tx(&bars[NST], D_HEAD * wrow);
   }
   __syncthreads();                                                  // barriers initialised
   {
@@ -190,8 +186,24 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
       bulk_g2s(reinterpret_cast<uint8_t*>(Ws) + row * WROWB, wsrc + (int64_t)row * p.rbits, wrow, &bars[NST]);
   }
   __syncthreads();                                                  // W_g requests ahead of the stream
-  if (tid == 0)
+  // Programmatic dependent launch: everything above reads only the hash
+  // weights (no preceding kernel produces them); q, k_new, v_new, n, the code
+  // cache (a preceding decode may append to it), the workspace and every
+  // global write come after the wait.  A no-op without the launch attribute.
+  griddep_wait();
+  const int64_t n = p.n[b];
+  if (tid == 0) {
+    // q and the new key/value first (they gate the q-hash), then the code
+    // chunk in a few large copies: a CTA's TMA requests are served in order
+    const uint32_t qbytes = (uint32_t)(G * D_HEAD * EB), kbytes = append ? (uint32_t)(D_HEAD * EB) : 0u;
+    mbar_arrive_expect_tx(&bars[NST + 1], qbytes + 2 * kbytes);
+    bulk_g2s(qraw, qg, qbytes, &bars[NST + 1]);
+    if (kbytes) {                                                   // new key and value rows
+      bulk_g2s(qraw + G * D_HEAD, reinterpret_cast<const T*>(p.k_new) + (int64_t)u * D_HEAD, kbytes, &bars[NST + 1]);
+      bulk_g2s(qraw + (G + 1) * D_HEAD, reinterpret_cast<const T*>(p.v_new) + (int64_t)u * D_HEAD, kbytes, &bars[NST + 1]);
+    }
     for (int s = 0; s < NST && s < nstages; ++s) issue_stage(s);
+  }
   for (int i = tid; i < p.nbins; i += DEC_THREADS) hist[i] = 0;
   const int kp = (int)(n < (int64_t)p.k ? n : (int64_t)p.k);      // k' = min(k, n)  (R10)
   auto chunk_len = [&](int rr) -> int {                            // valid tokens of rank rr
@@ -208,7 +220,8 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
   const int64_t pos = n - 1;
   const bool owner = append && n >= 1 && pos >= t0 && pos < t0 + Lr;
   const int NV = G + (owner ? 1 : 0);                                // projected vectors
-  mbar_wait(&bars[NST], 0);                                         // W_g, q, k_new in smem
+  mbar_wait(&bars[NST], 0);                                         // W_g in smem
+  mbar_wait(&bars[NST + 1], 0);                                     // q, k_new, v_new in smem
   HATA_TRACE(9);
   if constexpr (EB != 2)                                            // fp32 paths read q as floats
     for (int i = tid; i < NV * D_HEAD; i += DEC_THREADS) qf[(i / D_HEAD) * QS + i % D_HEAD] = Elem<T>::to_f(qraw[i]);
@@ -487,8 +500,8 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
     if (tid == 0) red_add_release_gpu(sync, 1u);   // release the CTA's writes (cumulative over bar.sync)
     HATA_TRACE(27);
     if (tid == 0) {
-      while (ld_acquire_gpu(sync) < (unsigned)M) {
-      }
+      for (unsigned spins = 0; ld_acquire_gpu(sync) < (unsigned)M;)
+        if (++spins > HATA_SPIN_LIMIT) __trap();                     // a lost arrival: fail loudly, never hang
       // the owner's K/V row (generic stores) -> this CTA's gather (async proxy)
       asm volatile("fence.proxy.async.global;" ::: "memory");
     }
