@@ -29,6 +29,9 @@ constexpr int DEC_STAGE_BYTES = 32768;       // one bulk copy of codes (few larg
 constexpr int DEC_MAX_STAGES = 4;            // code ring depth (up to 128 KB in flight)
 constexpr int DEC_D_SMEM_MAX = 16384;        // tokens/CTA whose D (u16) stays in smem
 constexpr int DEC_CHUNK_ALIGN = 64;          // tokens
+constexpr int DEC_BC_WPT = 2;               // candidate-bitmap words per thread (fast selection path)
+constexpr int DEC_HINT_SLACK = 2;           // hint threshold slack (bins)
+constexpr int DEC_WIN = 8;                  // bins [Th - 6, Th + 1] of every rank's prefix counts read with the totals
 constexpr int DEC_MAX_RANKS = 32;            // M cap (histogram exchange is M x nbins per rank)
 constexpr int DEC_ROW_PAD = 16;              // bytes of padding per staged K/V row (bank spread)
 constexpr int DEC_QS_PAD = 4;                // floats of padding per q row in smem
@@ -67,7 +70,7 @@ struct DecodeParams {
   int32_t* ws_tot;         // [units, hs] sum over the ranks of cum_r (atomics)        (M > 1)
   uint16_t* ws_D;          // [units, M, chunk] D when it does not fit in smem (!d_smem)
   float* ws_part;          // [units, M, GT, d+2]          (M > 1)
-  unsigned* ws_sync;       // [units, 2]: barrier, done    (M > 1)
+  unsigned* ws_sync;       // [units, 4]: barrier, done, threshold hint, -   (M > 1)
   // sequence-shard phase 1 (hata_shard_candidates): stop after the select and
   // emit (D, global index) candidates instead of attending.
   int cand_mode;
@@ -80,10 +83,11 @@ struct DecodeParams {
   const void* v_new;
   unsigned long long* trace;   // diagnostics (hata_debug_trace), null = off
   int dbg;                     // diagnostics: HATA_DEBUG bits (0 in production)
+  int use_hint;                // threshold hint from the previous launch (HATA_HINT=0 disables)
 };
 
 struct DecodeSmem {
-  int ring, W, bars, hist, D, qf, qw, planes, rows, red, misc, chref, total;
+  int ring, W, bars, hist, D, bc, qf, qw, planes, rows, red, misc, chref, total;
   int qp;                  // q-projection partial sums [DEC_THREADS/rbits][GT][rbits]
   int qraw;                // q rows (+ the new key) as stored, bulk-copied
   int hm, kv, sc, rb;      // aliases inside ring+W after scoring
@@ -148,6 +152,7 @@ __host__ __device__ inline DecodeSmem decode_smem_layout(const DecodeParams& p, 
   s.bars = off; off += up((DEC_MAX_STAGES + 4) * 8);
   s.hist = off; off += up(p.nbins * 4);
   s.D = off; off += p.d_smem ? up(dec_dchunk(p.chunk) * 2) : 0;
+  s.bc = off; off += p.d_smem ? up(dec_dchunk(p.chunk) / 8) : 0;   // candidate bitmap (1 bit per token)
   s.qf = off; off += up((GT + 1) * dec_qstride(p.d) * 4);
   s.qw = off; off += up((GT + 1) * (p.rbits / 32) * 4);
   s.qraw = off; off += up((GT + 2) * p.d * eb);   // q rows, new key, new value

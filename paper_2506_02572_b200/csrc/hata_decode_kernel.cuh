@@ -143,6 +143,7 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
   int32_t* rows = p.ws_rows ? p.ws_rows + ((int64_t)u * M + r) * p.R_cap : reinterpret_cast<int32_t*>(smem + L.rows);
   int32_t* red = reinterpret_cast<int32_t*>(smem + L.red);
   int32_t* misc = reinterpret_cast<int32_t*>(smem + L.misc);
+  int32_t* win = reinterpret_cast<int32_t*>(smem + L.chref);       // [M][DEC_WIN] prefix counts near the hint
   float* fmisc = reinterpret_cast<float*>(misc);
 
   // Rank chunks [rr*per, (rr+1)*per) are fixed by the host from n_max, so the
@@ -196,8 +197,9 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
     // q and the new key/value first (they gate the q-hash), then the code
     // chunk in a few large copies: a CTA's TMA requests are served in order
     const uint32_t qbytes = (uint32_t)(G * D_HEAD * EB), kbytes = append ? (uint32_t)(D_HEAD * EB) : 0u;
-    mbar_arrive_expect_tx(&bars[NST + 1], qbytes + 2 * kbytes);
+    mbar_arrive_expect_tx(&bars[NST + 1], qbytes + 2 * kbytes + (M > 1 ? 16u : 0u));
     bulk_g2s(qraw, qg, qbytes, &bars[NST + 1]);
+    if (M > 1) bulk_g2s(misc + 12, p.ws_sync + 4 * u, 16u, &bars[NST + 1]);   // [14] = threshold hint
     if (kbytes) {                                                   // new key and value rows
       bulk_g2s(qraw + G * D_HEAD, reinterpret_cast<const T*>(p.k_new) + (int64_t)u * D_HEAD, kbytes, &bars[NST + 1]);
       bulk_g2s(qraw + (G + 1) * D_HEAD, reinterpret_cast<const T*>(p.v_new) + (int64_t)u * D_HEAD, kbytes, &bars[NST + 1]);
@@ -205,6 +207,15 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
     for (int s = 0; s < NST && s < nstages; ++s) issue_stage(s);
   }
   for (int i = tid; i < p.nbins; i += DEC_THREADS) hist[i] = 0;
+  // Candidate hint: the unit's threshold of the previous launch on this
+  // workspace (+ DEC_HINT_SLACK).  Tokens with D <= Th are marked in a bitmap
+  // while the ranks exchange counts, so that when this launch's threshold is <= Th the
+  // selection visits only the marked tokens; otherwise it scans all of D.
+  // A hint changes the work done, never the result.
+  uint32_t* Bc = reinterpret_cast<uint32_t*>(smem + L.bc);
+  const int nbw = p.d_smem ? dec_dchunk(p.chunk) / 32 : 0;          // bitmap words
+  int Th = -1;
+  const bool hinted = p.use_hint && M > 1 && nbw > 0 && nbw <= DEC_BC_WPT * DEC_THREADS;
   const int kp = (int)(n < (int64_t)p.k ? n : (int64_t)p.k);      // k' = min(k, n)  (R10)
   auto chunk_len = [&](int rr) -> int {                            // valid tokens of rank rr
     const int64_t a = (int64_t)rr * per, z = min((int64_t)n, a + per);
@@ -221,7 +232,8 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
   const bool owner = append && n >= 1 && pos >= t0 && pos < t0 + Lr;
   const int NV = G + (owner ? 1 : 0);                                // projected vectors
   mbar_wait(&bars[NST], 0);                                         // W_g in smem
-  mbar_wait(&bars[NST + 1], 0);                                     // q, k_new, v_new in smem
+  mbar_wait(&bars[NST + 1], 0);                                     // q, k_new, v_new (+ hint) in smem
+  if (hinted) { const int h = misc[14]; Th = h > 0 ? h + DEC_HINT_SLACK : -1; }
   HATA_TRACE(9);
   if constexpr (EB != 2)                                            // fp32 paths read q as floats
     for (int i = tid; i < NV * D_HEAD; i += DEC_THREADS) qf[(i / D_HEAD) * QS + i % D_HEAD] = Elem<T>::to_f(qraw[i]);
@@ -465,7 +477,7 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
   // quota and the output position of its first selected token), then
   // compacts its OWN selected tokens in order and attends to them.
   const int hs = dec_hist_stride(p.nbins + 1);
-  unsigned* sync = (M > 1) ? p.ws_sync + 2 * u : nullptr;
+  unsigned* sync = (M > 1) ? p.ws_sync + 4 * u : nullptr;
   HATA_TRACE(2);
   constexpr int BPT_MAX = (8 * 256 + 1 + DEC_THREADS) / DEC_THREADS;  // nbins + 1 <= G*rbits + 2 (G <= 8, rbits <= 256)
   const int BPT = (p.nbins + DEC_THREADS) / DEC_THREADS;
@@ -498,6 +510,25 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
     }
     __syncthreads();
     if (tid == 0) red_add_release_gpu(sync, 1u);   // release the CTA's writes (cumulative over bar.sync)
+    if (Th >= 0) {
+      // candidate bitmap while the other ranks arrive: thread t owns words
+      // [t*WPT, (t+1)*WPT) (32 tokens each); bit i of word w = (D[32w+i] <= Th)
+      const uint32_t th_k = (uint32_t)Th * 0x10001u + 0x80008000u;
+      const int WPT = (nbw + DEC_THREADS - 1) / DEC_THREADS;
+      for (int w = tid * WPT; w < min(nbw, (tid + 1) * WPT); ++w) {
+        const uint4* dq = reinterpret_cast<const uint4*>(Dloc + 32 * w);
+        uint32_t m = 0u;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const uint4 x = dq[c];
+          const uint32_t a0 = (th_k - x.x) & 0x80008000u, a1 = (th_k - x.y) & 0x80008000u;
+          const uint32_t a2 = (th_k - x.z) & 0x80008000u, a3 = (th_k - x.w) & 0x80008000u;
+          m |= (((a0 >> 15) & 1u) | ((a0 >> 30) & 2u) | ((a1 >> 13) & 4u) | ((a1 >> 28) & 8u) |
+                ((a2 >> 11) & 16u) | ((a2 >> 26) & 32u) | ((a3 >> 9) & 64u) | ((a3 >> 24) & 128u)) << (8 * c);
+        }
+        Bc[w] = m;
+      }
+    }
     HATA_TRACE(27);
     if (tid == 0) {
       for (unsigned spins = 0; ld_acquire_gpu(sync) < (unsigned)M;)
@@ -507,6 +538,15 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
     }
     __syncthreads();
     HATA_TRACE(3);
+    // with a hint, the ranks' prefix counts at the bins around it come in the
+    // same round trip as the totals (the tie quota then needs no second one)
+    // (loaded here, stored after the totals' loads are issued)
+    int wv = 0;
+    const bool wl = Th >= 0 && tid < M * DEC_WIN;
+    if (wl) {
+      const int rr = tid / DEC_WIN, bi = Th - (DEC_WIN - 2) + tid % DEC_WIN;
+      if (bi >= 0 && bi <= p.nbins) wv = __ldcg(p.ws_hist + ((int64_t)u * M + rr) * hs + bi);
+    }
     // thr: the bin where the unit's cumulative count crosses k'
 #pragma unroll
     for (int q = 0; q < BPT_MAX; ++q) {
@@ -516,6 +556,7 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
         if (a < kp && kp <= z) { misc[0] = i; misc[1] = kp - a; }
       }
     }
+    if (wl) win[tid] = wv;
   } else {
     HATA_TRACE(3);
     int c = cum;
@@ -528,15 +569,22 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
   __syncthreads();
   const int thr = misc[0];
   const int need = misc[1];
+  if (M > 1 && r == 0 && tid == 0) reinterpret_cast<int*>(p.ws_sync)[4 * u + 2] = thr;   // next launch's hint
   // this rank's tie quota and the selection position of its first token
   // (computed by every warp: no further barrier); the loads are issued here
   // and consumed after the counting pass below
   int quota = need, off0 = 0;
   int bl = 0, ti = 0;
   if (M > 1 && thr >= 0 && lane < M) {
-    const int32_t* cr = p.ws_hist + ((int64_t)u * M + lane) * hs;
-    bl = __ldcg(cr + thr);
-    ti = __ldcg(cr + thr + 1);
+    const int w0 = Th - (DEC_WIN - 2);                                // window bins [w0, w0 + DEC_WIN)
+    if (Th >= 0 && thr >= w0 && thr + 1 < w0 + DEC_WIN) {
+      bl = win[lane * DEC_WIN + thr - w0];
+      ti = win[lane * DEC_WIN + thr + 1 - w0];
+    } else {
+      const int32_t* cr = p.ws_hist + ((int64_t)u * M + lane) * hs;
+      bl = __ldcg(cr + thr);
+      ti = __ldcg(cr + thr + 1);
+    }
   }
   HATA_TRACE(11);
   HATA_CLK(0);
@@ -557,104 +605,162 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
   // ((x | 0x8000) - d) keeps bit 15 iff d <= x, with no borrow between halves
   const uint32_t lt_k = thr >= 1 ? (uint32_t)(thr - 1) * 0x10001u + 0x80008000u : 0u;   // d <  thr
   const uint32_t le_k = thr >= 0 ? (uint32_t)thr * 0x10001u + 0x80008000u : 0u;         // d <= thr
+  // 8-bit mask of a block of 8 tokens from 4 SWAR mask words, bit i = token i
+  auto pack8 = [](const uint32_t (&m)[4]) -> uint32_t {
+    return ((m[0] >> 15) & 1u) | ((m[0] >> 30) & 2u) | ((m[1] >> 13) & 4u) | ((m[1] >> 28) & 8u) |
+           ((m[2] >> 11) & 16u) | ((m[2] >> 26) & 32u) | ((m[3] >> 9) & 64u) | ((m[3] >> 24) & 128u);
+  };
   auto swar = [&](uint32_t w, uint32_t& ltw, uint32_t& eqw) {
     ltw = thr >= 1 ? (lt_k - w) & 0x80008000u : 0u;
     const uint32_t lew = thr >= 0 ? (le_k - w) & 0x80008000u : 0u;
     eqw = lew & ~ltw;
   };
-  int lt_m = 0, eq_m = 0;
-  if (thr >= 0) {
-#pragma unroll 4
-    for (int c = 0; c < S8; ++c) {
-      const uint4 x = Dv[c];
-      uint32_t l0, e0, l1, e1, l2, e2, l3, e3;
-      swar(x.x, l0, e0); swar(x.y, l1, e1); swar(x.z, l2, e2); swar(x.w, l3, e3);
-      lt_m += __popc(l0) + __popc(l1) + __popc(l2) + __popc(l3);
-      eq_m += __popc(e0) + __popc(e1) + __popc(e2) + __popc(e3);
+  // this rank's tie quota and output offset from the M ranks' prefix counts
+  // at thr, thr+1 (lane i: rank i); every warp computes the same values
+  auto compute_quota = [&]() {
+    if (M > 1 && thr >= 0) {
+      ti -= bl;
+      int incl = ti;
+  #pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+      }
+      const int qv = max(0, min(need - (incl - ti), ti));
+      const int sel = bl + qv;
+      int inc2 = sel;
+  #pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, inc2, o);
+        if (lane >= o) inc2 += v;
+      }
+      quota = __shfl_sync(0xffffffffu, qv, r);
+      off0 = __shfl_sync(0xffffffffu, inc2 - sel, r);
     }
-  }
-  HATA_CLK(1);
-  // warp-inclusive scans of both counts
-  int lt_i = lt_m, eq_i = eq_m;
+  };
+  int Rr = 0;
+  // fast path: this launch's threshold is covered by the hint, so every
+  // token with D <= thr is marked in Bc; thread t owns the bitmap words
+  // [t*WPT, (t+1)*WPT) (token order), visits only the marked tokens, and the
+  // picks are emitted in token order from one block scan of the counts
+  const bool fast = Th >= 0 && thr >= 0 && thr <= Th;
+  if (fast) {
+    const int WPT = (nbw + DEC_THREADS - 1) / DEC_THREADS;
+    uint32_t ltw[DEC_BC_WPT], eqw[DEC_BC_WPT];
+    int nlt = 0, neq = 0;
 #pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int a = __shfl_up_sync(0xffffffffu, lt_i, o), e = __shfl_up_sync(0xffffffffu, eq_i, o);
-    if (lane >= o) { lt_i += a; eq_i += e; }
-  }
-  int* wcnt = misc + 16;                                            // [DEC_WARPS][2] warp totals
-  if (lane == 31) { wcnt[2 * warp] = lt_i; wcnt[2 * warp + 1] = eq_i; }
-  HATA_CLK(2);
-  HATA_TRACE(18);
-  if (M > 1 && thr >= 0) {
-    ti -= bl;
-    int incl = ti;
+    for (int j = 0; j < DEC_BC_WPT; ++j) {
+      const int w = tid * WPT + j;
+      uint32_t lt = 0u, eq = 0u;
+      if (j < WPT && w < nbw && Bc[w]) {
+        // the word's 32 distances by SWAR (bounded cost for dense words)
+        const uint4* dq = reinterpret_cast<const uint4*>(Dloc + 32 * w);
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int v = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += v;
-    }
-    const int qv = max(0, min(need - (incl - ti), ti));
-    const int sel = bl + qv;
-    int inc2 = sel;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int v = __shfl_up_sync(0xffffffffu, inc2, o);
-      if (lane >= o) inc2 += v;
-    }
-    quota = __shfl_sync(0xffffffffu, qv, r);
-    off0 = __shfl_sync(0xffffffffu, inc2 - sel, r);
-  }
-  HATA_CLK(3);
-  __syncthreads();
-  HATA_CLK(4);
-  // this thread's exclusive offsets within the rank, and the rank totals
-  int lt_b = lt_i - lt_m, ti_b = eq_i - eq_m, lt_tot = 0, ti_tot = 0;
-#pragma unroll
-  for (int w = 0; w < DEC_WARPS; ++w) {
-    const int cl = wcnt[2 * w], ct = wcnt[2 * w + 1];
-    if (w < warp) { lt_b += cl; ti_b += ct; }
-    lt_tot += cl;
-    ti_tot += ct;
-  }
-  const int Rr = lt_tot + min(ti_tot, quota);                       // rows this rank attends to
-  HATA_CLK(5);
-  HATA_TRACE(21);
-  if (thr >= 0 && lt_m + min(max(quota - ti_b, 0), eq_m) > 0) {
-    for (int c = 0; c < S8; ++c) {
-      const uint4 x = Dv[c];
-      uint32_t lw[4], ew[4];
-      swar(x.x, lw[0], ew[0]); swar(x.y, lw[1], ew[1]); swar(x.z, lw[2], ew[2]); swar(x.w, lw[3], ew[3]);
-      // 8-bit masks of the block, bit i = token i (word i/2, half i%2)
-      auto pack8 = [](const uint32_t (&m)[4]) -> uint32_t {
-        return ((m[0] >> 15) & 1u) | ((m[0] >> 30) & 2u) | ((m[1] >> 13) & 4u) | ((m[1] >> 28) & 8u) |
-               ((m[2] >> 11) & 16u) | ((m[2] >> 26) & 32u) | ((m[3] >> 9) & 64u) | ((m[3] >> 24) & 128u);
-      };
-      const uint32_t lt8 = pack8(lw), eq8 = pack8(ew);
-      if (lt8 | eq8) {
-        // the first max(0, quota - ti_b) ties of the block are taken (R8)
-        uint32_t tie8 = 0u, e8 = eq8;
-        for (int take = min(__popc(eq8), max(quota - ti_b, 0)); take > 0; --take) {
-          tie8 |= e8 & (0u - e8);                                    // lowest remaining tie
-          e8 &= e8 - 1u;
+        for (int c = 0; c < 4; ++c) {
+          const uint4 x = dq[c];
+          uint32_t l4[4], e4[4];
+          swar(x.x, l4[0], e4[0]); swar(x.y, l4[1], e4[1]); swar(x.z, l4[2], e4[2]); swar(x.w, l4[3], e4[3]);
+          lt |= pack8(l4) << (8 * c);
+          eq |= pack8(e4) << (8 * c);
         }
-        const uint32_t sel8 = lt8 | tie8;
-        const int base = lt_b + min(ti_b, quota);                    // position of the block's first pick
-        // only the rows list is on the critical path; out_idx / out_score /
-        // cand_D are written from it after the attention (coalesced)
-        auto emit = [&](int pl, int i) { rows[pl] = (int32_t)t0 + (tid * S8 + c) * 8 + i; };
-        if (__popc(sel8) >= 3) {                                     // dense block (e.g. a recent window):
-          int rr = 0;                                                // predicated, no per-pick popc
+      }
+      ltw[j] = lt;
+      eqw[j] = eq;
+      nlt += __popc(lt);
+      neq += __popc(eq);
+    }
+    int ti_b, lt_tot, ti_tot;
+    int lt_b = block_excl_scan2(nlt, neq, misc + 16, ti_b, lt_tot, ti_tot);
+    compute_quota();
+    Rr = lt_tot + min(ti_tot, quota);
 #pragma unroll
-          for (int i = 0; i < 8; ++i)
-            if ((sel8 >> i) & 1u) emit(base + rr++, i);
-        } else {
-          for (uint32_t m = sel8; m; m &= m - 1u) {
-            const int i = __ffs(m) - 1;
-            emit(base + __popc(sel8 & ((1u << i) - 1u)), i);
+    for (int j = 0; j < DEC_BC_WPT; ++j) {
+      const int w = tid * WPT + j;
+      if (j < WPT && w < nbw && (ltw[j] | eqw[j])) {
+        // the first max(0, quota - ti_b) ties of the word are taken (R8)
+        uint32_t ties = 0u, e = eqw[j];
+        for (int take = min(__popc(e), max(quota - ti_b, 0)); take > 0; --take) {
+          ties |= e & (0u - e);
+          e &= e - 1u;
+        }
+        int pl = lt_b + min(ti_b, quota);
+        for (uint32_t sel = ltw[j] | ties; sel; sel &= sel - 1u) rows[pl++] = (int32_t)t0 + 32 * w + (__ffs(sel) - 1);
+        lt_b += __popc(ltw[j]);
+        ti_b += __popc(eqw[j]);
+      }
+    }
+  } else {
+    int lt_m = 0, eq_m = 0;
+    if (thr >= 0) {
+  #pragma unroll 4
+      for (int c = 0; c < S8; ++c) {
+        const uint4 x = Dv[c];
+        uint32_t l0, e0, l1, e1, l2, e2, l3, e3;
+        swar(x.x, l0, e0); swar(x.y, l1, e1); swar(x.z, l2, e2); swar(x.w, l3, e3);
+        lt_m += __popc(l0) + __popc(l1) + __popc(l2) + __popc(l3);
+        eq_m += __popc(e0) + __popc(e1) + __popc(e2) + __popc(e3);
+      }
+    }
+    HATA_CLK(1);
+    // warp-inclusive scans of both counts
+    int lt_i = lt_m, eq_i = eq_m;
+  #pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int a = __shfl_up_sync(0xffffffffu, lt_i, o), e = __shfl_up_sync(0xffffffffu, eq_i, o);
+      if (lane >= o) { lt_i += a; eq_i += e; }
+    }
+    int* wcnt = misc + 16;                                            // [DEC_WARPS][2] warp totals
+    if (lane == 31) { wcnt[2 * warp] = lt_i; wcnt[2 * warp + 1] = eq_i; }
+    HATA_CLK(2);
+    HATA_TRACE(18);
+    compute_quota();
+    HATA_CLK(3);
+    __syncthreads();
+    HATA_CLK(4);
+    // this thread's exclusive offsets within the rank, and the rank totals
+    int lt_b = lt_i - lt_m, ti_b = eq_i - eq_m, lt_tot = 0, ti_tot = 0;
+  #pragma unroll
+    for (int w = 0; w < DEC_WARPS; ++w) {
+      const int cl = wcnt[2 * w], ct = wcnt[2 * w + 1];
+      if (w < warp) { lt_b += cl; ti_b += ct; }
+      lt_tot += cl;
+      ti_tot += ct;
+    }
+    Rr = lt_tot + min(ti_tot, quota);                                 // rows this rank attends to
+    HATA_CLK(5);
+    HATA_TRACE(21);
+    if (thr >= 0 && lt_m + min(max(quota - ti_b, 0), eq_m) > 0) {
+      for (int c = 0; c < S8; ++c) {
+        const uint4 x = Dv[c];
+        uint32_t lw[4], ew[4];
+        swar(x.x, lw[0], ew[0]); swar(x.y, lw[1], ew[1]); swar(x.z, lw[2], ew[2]); swar(x.w, lw[3], ew[3]);
+        const uint32_t lt8 = pack8(lw), eq8 = pack8(ew);
+        if (lt8 | eq8) {
+          // the first max(0, quota - ti_b) ties of the block are taken (R8)
+          uint32_t tie8 = 0u, e8 = eq8;
+          for (int take = min(__popc(eq8), max(quota - ti_b, 0)); take > 0; --take) {
+            tie8 |= e8 & (0u - e8);                                    // lowest remaining tie
+            e8 &= e8 - 1u;
           }
+          const uint32_t sel8 = lt8 | tie8;
+          const int base = lt_b + min(ti_b, quota);                    // position of the block's first pick
+          // only the rows list is on the critical path; out_idx / out_score /
+          // cand_D are written from it after the attention (coalesced)
+          auto emit = [&](int pl, int i) { rows[pl] = (int32_t)t0 + (tid * S8 + c) * 8 + i; };
+          if (__popc(sel8) >= 3) {                                     // dense block (e.g. a recent window):
+            int rr = 0;                                                // predicated, no per-pick popc
+  #pragma unroll
+            for (int i = 0; i < 8; ++i)
+              if ((sel8 >> i) & 1u) emit(base + rr++, i);
+          } else {
+            for (uint32_t m = sel8; m; m &= m - 1u) {
+              const int i = __ffs(m) - 1;
+              emit(base + __popc(sel8 & ((1u << i) - 1u)), i);
+            }
+          }
+          lt_b += __popc(lt8);
+          ti_b += __popc(eq8);
         }
-        lt_b += __popc(lt8);
-        ti_b += __popc(eq8);
       }
     }
   }

@@ -18,9 +18,11 @@ def codes_u32(t: torch.Tensor) -> np.ndarray:
     return t.detach().cpu().numpy().view(np.uint32)
 
 
-def gpu_step(case: dict, k: int, n_override=None, out_dtype=torch.float32, device="cuda", fused=False):
+def gpu_step(case: dict, k: int, n_override=None, out_dtype=torch.float32, device="cuda", fused=False,
+             workspace=None):
     """prefill-hash rows [0, N-1), append row n_before, decode; all via the C ABI.
-    fused=True runs append + decode as one hata_decode_step launch."""
+    fused=True runs append + decode as one hata_decode_step launch.  A reused
+    workspace carries the previous launch's threshold hint (fast selection)."""
     import paper_2506_02572_b200 as H
     sh = case["shape"]
     q = case["q"].to(device)
@@ -40,11 +42,11 @@ def gpu_step(case: dict, k: int, n_override=None, out_dtype=torch.float32, devic
     qcodes = torch.zeros(B, sh.Hq, Wd, dtype=torch.int32, device=device)
     if fused:
         out = H.decode_step(q, kn, vn, K, V, codes, W, n, k, n_max=n_max, out_dtype=out_dtype, out_idx=out_idx,
-                            out_score=out_score, out_qcodes=qcodes)
+                            out_score=out_score, out_qcodes=qcodes, workspace=workspace)
     else:
         H.append(kn, vn, W, K, V, codes, nb)
         out = H.decode_topk_attn(q, K, V, codes, W, n, k, n_max=n_max, out_dtype=out_dtype, out_idx=out_idx,
-                                 out_score=out_score, out_qcodes=qcodes)
+                                 out_score=out_score, out_qcodes=qcodes, workspace=workspace)
     torch.cuda.synchronize()
     return dict(K=K.cpu(), V=V.cpu(), codes=codes.cpu(), out=out.cpu(), idx=out_idx.cpu(),
                 score=out_score.cpu(), qc=qcodes.cpu(), n=n.cpu())

@@ -81,3 +81,47 @@ def test_bf16_output_dtype():
     g16 = gpu_step(case, shape.k, out_dtype=torch.bfloat16)
     assert torch.equal(g32["idx"], g16["idx"])
     assert (g16["out"].float() - g32["out"]).abs().max().item() <= 2 ** -8 * g32["out"].abs().max().item() + 1e-6
+
+
+def _ws_for(shape, k):
+    import paper_2506_02572_b200 as H
+    dt = torch.bfloat16 if shape.dtype == "bf16" else torch.float32
+    n = shape.N
+    ws = H.decode_workspace_size(shape.B, shape.Hq, shape.Hkv, shape.d, shape.rbits, n, k, dt)
+    return torch.zeros(max(ws, 1), dtype=torch.uint8, device="cuda")
+
+
+HINTED = [
+    ("g4_r128_8k", _shape("cfg2", N=8192 + 37, k=256), "planted"),
+    ("g5_r256_small", _shape("cfg5", B=2, N=6000, k=200), "planted"),
+    ("tie_pool8", _shape("cfg2", N=9000, k=700), "pool8"),
+    ("tie_dup", _shape("cfg2", N=8192, k=333), "dup"),
+    ("cfg2", synth.CONFIGS["cfg2"], "planted"),
+]
+
+
+@pytest.mark.parametrize("name,shape,variant", HINTED, ids=[s[0] for s in HINTED])
+def test_decode_parity_hinted(name, shape, variant):
+    """A reused workspace holds the previous launch's threshold: the second
+    launch takes the candidate-bitmap selection; results must not change."""
+    ws = _ws_for(shape, shape.k)
+    case = synth.make_case(shape, seed=13, variant=variant)
+    for _ in range(3):
+        g = gpu_step(case, shape.k, fused=True, workspace=ws)
+        st = check_decode(case, g, shape.k)
+    print(name, st)
+
+
+@pytest.mark.parametrize("first,second", [("planted", "pool8"), ("pool8", "planted"), ("planted", "dup"),
+                                          ("dup", "planted"), ("equal", "planted"), ("planted", "equal")])
+def test_decode_parity_stale_hint(first, second):
+    """The hint comes from a different problem (higher or lower threshold):
+    the selection falls back or scans extra candidates, never changes."""
+    shape = _shape("cfg2", N=12000, k=600)
+    ws = _ws_for(shape, shape.k)
+    a = synth.make_case(shape, seed=21, variant=first)
+    gpu_step(a, shape.k, fused=True, workspace=ws)
+    b = synth.make_case(shape, seed=22, variant=second)
+    g = gpu_step(b, shape.k, fused=True, workspace=ws)
+    st = check_decode(b, g, shape.k)
+    print(first, second, st)
