@@ -8,8 +8,9 @@
 // w owns tokens [16w, 16w+16).  K tiles and W_g are staged in smem (padded rows, so
 // the ldmatrix fragments are bank-conflict free); every 16 x 8 output tile is
 // one chain of D/16 mma.sync m16n8k16 (bf16 products are exact, fp32
-// accumulation, R13); the sign bits are packed straight from the accumulator
-// fragments by ballots into LSB-first uint32 words (R6, R7).
+// accumulation, R13), four chains per code word; each lane packs the sign bits
+// of its accumulator fragments into its 2 bits per n-tile of the LSB-first
+// uint32 word and the 4 lanes of a row OR-reduce by shuffles (R6, R7).
 //
 // This is the legacy-MMA (HMMA) path: at rbits = 128 the projection needs
 // 128 flop per K byte, so HMMA (~0.58 PFLOP/s on this part) rather than HBM
@@ -82,33 +83,33 @@ __global__ void __launch_bounds__(HK_THREADS) hash_keys_mma_kernel(const HashKey
     }
     uint32_t wlo[W], whi[W];                  // code words of rows gid and gid + 8
 #pragma unroll
-    for (int w = 0; w < W; ++w) wlo[w] = whi[w] = 0u;
+    for (int w = 0; w < W; ++w) {
+      // one code word = 4 output n-tiles: 4 independent accumulator chains
+      float c[4][4];
 #pragma unroll
-    for (int nt0 = 0; nt0 < RB / 8; nt0 += 2) {   // two independent accumulator chains
-      float c[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+      for (int q = 0; q < 4; ++q) c[q][0] = c[q][1] = c[q][2] = c[q][3] = 0.f;
 #pragma unroll
       for (int ks = 0; ks < KS; ++ks)
 #pragma unroll
-        for (int q = 0; q < 2; ++q) {
+        for (int q = 0; q < 4; ++q) {
           uint32_t b0, b1;
-          ldsm_x2_trans(b0, b1, ws + (ks * 16 + (lane & 15)) * WROW + (nt0 + q) * 16);
+          ldsm_x2_trans(b0, b1, ws + (ks * 16 + (lane & 15)) * WROW + (4 * w + q) * 16);
           mma_bf16_16816(c[q], a[ks], b0, b1);
         }
+      // c0, c1: row gid, bits 8q + 2 tig (+1) of the word; c2, c3: row gid + 8.
+      // Each lane sets its 2 bits per n-tile; the 4 lanes of a row OR-reduce.
+      uint32_t lo = 0u, hi = 0u;
 #pragma unroll
-      for (int q = 0; q < 2; ++q) {
-        const int nt = nt0 + q;
-        // c0, c1: row gid, bits nt*8 + 2 tig (+1); c2, c3: row gid + 8
-        const uint32_t m0 = __ballot_sync(0xffffffffu, c[q][0] >= 0.f), m1 = __ballot_sync(0xffffffffu, c[q][1] >= 0.f);
-        const uint32_t m2 = __ballot_sync(0xffffffffu, c[q][2] >= 0.f), m3 = __ballot_sync(0xffffffffu, c[q][3] >= 0.f);
-        uint32_t lo = 0, hi = 0;              // bits nt*8 .. nt*8+7 of rows gid / gid+8, LSB-first (R7)
-#pragma unroll
-        for (int t = 0; t < 4; ++t) {
-          lo |= ((m0 >> (gid * 4 + t)) & 1u) << (2 * t) | ((m1 >> (gid * 4 + t)) & 1u) << (2 * t + 1);
-          hi |= ((m2 >> (gid * 4 + t)) & 1u) << (2 * t) | ((m3 >> (gid * 4 + t)) & 1u) << (2 * t + 1);
-        }
-        wlo[nt / 4] |= lo << (8 * (nt % 4));
-        whi[nt / 4] |= hi << (8 * (nt % 4));
+      for (int q = 0; q < 4; ++q) {
+        lo |= ((uint32_t)(c[q][0] >= 0.f) | ((uint32_t)(c[q][1] >= 0.f) << 1)) << (8 * q + 2 * tig);
+        hi |= ((uint32_t)(c[q][2] >= 0.f) | ((uint32_t)(c[q][3] >= 0.f) << 1)) << (8 * q + 2 * tig);
       }
+      lo |= __shfl_xor_sync(0xffffffffu, lo, 1);
+      hi |= __shfl_xor_sync(0xffffffffu, hi, 1);
+      lo |= __shfl_xor_sync(0xffffffffu, lo, 2);
+      hi |= __shfl_xor_sync(0xffffffffu, hi, 2);
+      wlo[w] = lo;
+      whi[w] = hi;
     }
     if (tig == 0) {
       const int64_t tbase = p.t0 + (int64_t)tile * HK_TOK;
