@@ -20,8 +20,9 @@
 
 namespace hata {
 
-constexpr int HK_TOK = 128;                  // tokens per CTA
-constexpr int HK_THREADS = 256;
+constexpr int HK_MT = 2;                     // 16-token m-tiles per warp (share every W_g fragment)
+constexpr int HK_THREADS = 128;
+constexpr int HK_TOK = HK_THREADS / 32 * 16 * HK_MT;   // tokens per CTA tile (128)
 
 // Persistent CTAs: CTA (x, u) hashes token tiles x, x + nx, x + 2 nx, ... of
 // unit u = (b, g); W_g is staged once, K tiles are double-buffered with
@@ -73,55 +74,66 @@ __global__ void __launch_bounds__(HK_THREADS) hash_keys_mma_kernel(const HashKey
     __syncthreads();
 
     constexpr int KS = D / 16;
-    uint32_t a[KS][4];
+    uint32_t a[HK_MT][KS][4];
 #pragma unroll
-    for (int ks = 0; ks < KS; ++ks) {
-      const uint8_t* ap = xs + (warp * 16 + (lane & 15)) * XROW + ks * 32 + (lane >> 4) * 16;
-      asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0, %1, %2, %3}, [%4];"
-                   : "=r"(a[ks][0]), "=r"(a[ks][1]), "=r"(a[ks][2]), "=r"(a[ks][3])
-                   : "r"(smem_u32(ap)));
-    }
-    uint32_t wlo[W], whi[W];                  // code words of rows gid and gid + 8
+    for (int mt = 0; mt < HK_MT; ++mt)
+#pragma unroll
+      for (int ks = 0; ks < KS; ++ks) {
+        const uint8_t* ap = xs + ((warp * HK_MT + mt) * 16 + (lane & 15)) * XROW + ks * 32 + (lane >> 4) * 16;
+        asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(a[mt][ks][0]), "=r"(a[mt][ks][1]), "=r"(a[mt][ks][2]), "=r"(a[mt][ks][3])
+                     : "r"(smem_u32(ap)));
+      }
+    uint32_t wlo[HK_MT][W], whi[HK_MT][W];    // code words of rows gid and gid + 8 of each m-tile
 #pragma unroll
     for (int w = 0; w < W; ++w) {
-      // one code word = 4 output n-tiles: 4 independent accumulator chains
-      float c[4][4];
+      // one code word = 4 output n-tiles: 4 x HK_MT independent accumulator chains
+      float c[HK_MT][4][4];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) c[q][0] = c[q][1] = c[q][2] = c[q][3] = 0.f;
+      for (int mt = 0; mt < HK_MT; ++mt)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) c[mt][q][0] = c[mt][q][1] = c[mt][q][2] = c[mt][q][3] = 0.f;
 #pragma unroll
       for (int ks = 0; ks < KS; ++ks)
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           uint32_t b0, b1;
           ldsm_x2_trans(b0, b1, ws + (ks * 16 + (lane & 15)) * WROW + (4 * w + q) * 16);
-          mma_bf16_16816(c[q], a[ks], b0, b1);
+#pragma unroll
+          for (int mt = 0; mt < HK_MT; ++mt) mma_bf16_16816(c[mt][q], a[mt][ks], b0, b1);
         }
       // c0, c1: row gid, bits 8q + 2 tig (+1) of the word; c2, c3: row gid + 8.
       // Each lane sets its 2 bits per n-tile; the 4 lanes of a row OR-reduce.
-      uint32_t lo = 0u, hi = 0u;
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        lo |= ((uint32_t)(c[q][0] >= 0.f) | ((uint32_t)(c[q][1] >= 0.f) << 1)) << (8 * q + 2 * tig);
-        hi |= ((uint32_t)(c[q][2] >= 0.f) | ((uint32_t)(c[q][3] >= 0.f) << 1)) << (8 * q + 2 * tig);
+      for (int mt = 0; mt < HK_MT; ++mt) {
+        uint32_t lo = 0u, hi = 0u;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          lo |= ((uint32_t)(c[mt][q][0] >= 0.f) | ((uint32_t)(c[mt][q][1] >= 0.f) << 1)) << (8 * q + 2 * tig);
+          hi |= ((uint32_t)(c[mt][q][2] >= 0.f) | ((uint32_t)(c[mt][q][3] >= 0.f) << 1)) << (8 * q + 2 * tig);
+        }
+        lo |= __shfl_xor_sync(0xffffffffu, lo, 1);
+        hi |= __shfl_xor_sync(0xffffffffu, hi, 1);
+        lo |= __shfl_xor_sync(0xffffffffu, lo, 2);
+        hi |= __shfl_xor_sync(0xffffffffu, hi, 2);
+        wlo[mt][w] = lo;
+        whi[mt][w] = hi;
       }
-      lo |= __shfl_xor_sync(0xffffffffu, lo, 1);
-      hi |= __shfl_xor_sync(0xffffffffu, hi, 1);
-      lo |= __shfl_xor_sync(0xffffffffu, lo, 2);
-      hi |= __shfl_xor_sync(0xffffffffu, hi, 2);
-      wlo[w] = lo;
-      whi[w] = hi;
     }
     if (tig == 0) {
       const int64_t tbase = p.t0 + (int64_t)tile * HK_TOK;
       const int ntok = (int)min((int64_t)HK_TOK, p.t0 + p.n - tbase);
-      const int r0 = warp * 16 + gid, r1 = r0 + 8;
-      if (r0 < ntok) {
 #pragma unroll
-        for (int w = 0; w < W; ++w) cb[(tbase + r0) * W + w] = wlo[w];
-      }
-      if (r1 < ntok) {
+      for (int mt = 0; mt < HK_MT; ++mt) {
+        const int r0 = (warp * HK_MT + mt) * 16 + gid, r1 = r0 + 8;
+        if (r0 < ntok) {
 #pragma unroll
-        for (int w = 0; w < W; ++w) cb[(tbase + r1) * W + w] = whi[w];
+          for (int w = 0; w < W; ++w) cb[(tbase + r0) * W + w] = wlo[mt][w];
+        }
+        if (r1 < ntok) {
+#pragma unroll
+          for (int w = 0; w < W; ++w) cb[(tbase + r1) * W + w] = whi[mt][w];
+        }
       }
     }
     __syncthreads();                          // this buffer is refilled two tiles on
