@@ -519,7 +519,11 @@ def main():
                    "l2": f"rotating {N_SETS} distinct cache sets ({N_SETS} x {bytes_step / 1e6:.1f} MB step bytes "
                          f"> 126 MB L2)", "parallelism": "single GPU",
                    "graph": f"{N_SETS} consecutive steps (one per cache set, like the attention layers of one "
-                            f"model decode step) per CUDA graph"},
+                            f"model decode step) per CUDA graph",
+                   "pdl": os.environ.get("HATA_PDL", "1") != "0",
+                   "pdl_note": "programmatic dependent launch: a step's barrier init + W_g loads overlap the previous "
+                               "step's tail; q, k_new, v_new, codes, workspace are read only after griddepcontrol.wait",
+                   "selection_hint": os.environ.get("HATA_HINT", "1") != "0"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": _ncu_traffic("hata_decode_kernel", sh.name), "traffic_source": "profiles/ncu_traffic.json (ncu dram__bytes_read+write per launch)",
                      "kernel": "hata_decode_kernel", "algorithmic_bytes_per_launch": bytes_step,
