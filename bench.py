@@ -537,7 +537,7 @@ def main():
     line["e2e"] = e2e
     if not args.no_secondary:
         sec = {}
-        for nm in ("cfg2",):
+        for nm in ("cfg2", "cfg3", "cfg5"):
             if nm == sh.name:
                 continue
             s2 = synth.CONFIGS[nm]
