@@ -31,7 +31,8 @@ import torch  # noqa: E402
 import synth  # noqa: E402
 
 METRIC = "decode attention µs/step & tokens/s at 32K/128K ctx; HBM GB/s vs roofline"
-N_SETS = int(os.environ.get("HATA_BENCH_SETS", "16"))   # < 8 is an L2-resident diagnostic, not a bench number
+N_SETS = int(os.environ.get("HATA_BENCH_SETS", "16"))
+KV_LAYOUT = os.environ.get("HATA_KV_LAYOUT", "pair")   # "pair": [B, H_kv, cap, 2, d]; "split": separate K and V   # < 8 is an L2-resident diagnostic, not a bench number
 
 
 def _peaks():
@@ -124,6 +125,12 @@ class Step:
         # planted rows (cheap on device): sinks + recent window get the group query direction
         self.sh = sh
         self.q, self.K, self.V, self.W = c["q"], c["K"], c["V"], c["W"]
+        if KV_LAYOUT == "pair" and self.K.dtype == torch.bfloat16:
+            # a token's K and V rows adjacent in HBM ([B, H_kv, cap, 2, d]):
+            # the decode gathers both with one 512-byte TMA request
+            kv = torch.stack((self.K, self.V), dim=3)
+            del c["K"], c["V"]
+            self.K, self.V = kv[:, :, :, 0, :], kv[:, :, :, 1, :]
         self.kn, self.vn = c["k_new"], c["v_new"]
         self.pos = c["n_before"]
         self.n = self.pos + 1
@@ -260,7 +267,7 @@ def bench_hash_keys(st, reps):
 def dense_baseline(st, steps):
     """Full-attention decode over the same cache (context, north_star)."""
     q = st.q.view(st.sh.B, st.sh.Hq, 1, st.sh.d)
-    K, V = st.K, st.V
+    K, V = st.K.contiguous(), st.V.contiguous()          # the dense kernel reads its own (split) layout
     try:
         from flash_attn import flash_attn_with_kvcache
         qf = st.q.view(st.sh.B, 1, st.sh.Hq, st.sh.d)
@@ -523,7 +530,9 @@ def main():
                    "pdl": os.environ.get("HATA_PDL", "1") != "0",
                    "pdl_note": "programmatic dependent launch: a step's barrier init + W_g loads overlap the previous "
                                "step's tail; q, k_new, v_new, codes, workspace are read only after griddepcontrol.wait",
-                   "selection_hint": os.environ.get("HATA_HINT", "1") != "0"},
+                   "selection_hint": os.environ.get("HATA_HINT", "1") != "0",
+                   "kv_layout": "[B, H_kv, cap, 2, d] (K and V rows of a token adjacent)" if KV_LAYOUT == "pair"
+                   else "separate K and V [B, H_kv, cap, d]"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": _ncu_traffic("hata_decode_kernel", sh.name), "traffic_source": "profiles/ncu_traffic.json (ncu dram__bytes_read+write per launch)",
                      "kernel": "hata_decode_kernel", "algorithmic_bytes_per_launch": bytes_step,

@@ -20,7 +20,7 @@ __device__ __forceinline__ void attend_rows_mma(const int32_t* rows, int Rr, con
                                                 const __nv_bfloat16* __restrict__ Vb, int64_t kv_st, const __nv_bfloat16* qb,
                                                 int G, float scale, uint8_t* kvbuf, int rows_cap, int rowb,
                                                 float* m_s, float* l_s, AttnState<GT, D_HEAD>& st,
-                                                uint64_t* bar, unsigned long long* tr = nullptr, int tb = 16) {
+                                                uint64_t* bar, int kvpair, unsigned long long* tr = nullptr, int tb = 16) {
   static_assert(GT <= 8, "heads per group <= 8");
   constexpr int CH = D_HEAD * 2 / 16;            // 16-byte chunks per row
   constexpr int KS = D_HEAD / 16;                // k-steps over the head dim
@@ -28,8 +28,12 @@ __device__ __forceinline__ void attend_rows_mma(const int32_t* rows, int Rr, con
   constexpr int NSL = AttnState<GT, D_HEAD>::NSL;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int gid = lane >> 2, tig = lane & 3;
+  // kvpair: the cache stores a token's K and V rows adjacently (V = K + d,
+  // row stride 2d): one 512-byte bulk copy per selected token lands [K|V]
+  // in one padded smem slot -- half the TMA requests of separate caches
+  if (kvpair) rowb = 2 * D_HEAD * 2 + DEC_ROW_PAD;
   uint8_t* Ks = kvbuf;
-  uint8_t* Vs = kvbuf + rows_cap * rowb;
+  uint8_t* Vs = kvpair ? kvbuf + D_HEAD * 2 : kvbuf + rows_cap * rowb;
 
   // Q as A fragments held in registers for the whole call, read once from the
   // bf16 rows as stored (qb: [G][D_HEAD] smem); heads >= G and rows 8..15 are zero
@@ -58,10 +62,15 @@ __device__ __forceinline__ void attend_rows_mma(const int32_t* rows, int Rr, con
     if (r0 == 0) HATA_TRACE_AT(tr, tb + 4);
     // request i -> warp i % NW, lane i / NW: a warp issues its bulk copies one
     // lane after another, so spread them over all warps
-    for (int i = lane * DEC_WARPS + warp; i < 2 * nb; i += DEC_THREADS) {
-      const int which = i >= nb, rr = i - (which ? nb : 0);
-      const __nv_bfloat16* src = (which ? Vb : Kb) + (int64_t)rows[r0 + rr] * kv_st;
-      bulk_g2s((which ? Vs : Ks) + rr * rowb, src, ROWBYTES, bar);
+    if (kvpair) {
+      for (int i = lane * DEC_WARPS + warp; i < nb; i += DEC_THREADS)
+        bulk_g2s(Ks + i * rowb, Kb + (int64_t)rows[r0 + i] * kv_st, 2 * ROWBYTES, bar);
+    } else {
+      for (int i = lane * DEC_WARPS + warp; i < 2 * nb; i += DEC_THREADS) {
+        const int which = i >= nb, rr = i - (which ? nb : 0);
+        const __nv_bfloat16* src = (which ? Vb : Kb) + (int64_t)rows[r0 + rr] * kv_st;
+        bulk_g2s((which ? Vs : Ks) + rr * rowb, src, ROWBYTES, bar);
+      }
     }
     if (r0 == 0) HATA_TRACE_AT(tr, tb + 3);
     mbar_wait(bar, bpar);

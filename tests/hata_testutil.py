@@ -19,7 +19,7 @@ def codes_u32(t: torch.Tensor) -> np.ndarray:
 
 
 def gpu_step(case: dict, k: int, n_override=None, out_dtype=torch.float32, device="cuda", fused=False,
-             workspace=None):
+             workspace=None, kv_pair=False):
     """prefill-hash rows [0, N-1), append row n_before, decode; all via the C ABI.
     fused=True runs append + decode as one hata_decode_step launch.  A reused
     workspace carries the previous launch's threshold hint (fast selection)."""
@@ -28,6 +28,9 @@ def gpu_step(case: dict, k: int, n_override=None, out_dtype=torch.float32, devic
     q = case["q"].to(device)
     K = case["K"].to(device).contiguous()
     V = case["V"].to(device).contiguous()
+    if kv_pair:   # K and V rows of a token adjacent: [B, H_kv, cap, 2, d]
+        kv = torch.stack((K, V), dim=3)
+        K, V = kv[:, :, :, 0, :], kv[:, :, :, 1, :]
     W = case["W"].to(device).contiguous()
     kn, vn = case["k_new"].to(device), case["v_new"].to(device)
     nb = (case["n_before"] if n_override is None else n_override).to(device)

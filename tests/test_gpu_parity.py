@@ -125,3 +125,23 @@ def test_decode_parity_stale_hint(first, second):
     g = gpu_step(b, shape.k, fused=True, workspace=ws)
     st = check_decode(b, g, shape.k)
     print(first, second, st)
+
+
+KVPAIR = [
+    ("g4_r128_8k", _shape("cfg2", N=8192 + 37, k=256), "planted"),
+    ("g5_r256_small", _shape("cfg5", B=2, N=6000, k=200), "planted"),
+    ("g8_r128", _shape("cfg2", Hq=64, Hkv=8, N=4000, k=129), "planted"),
+    ("tie_pool8", _shape("cfg2", N=9000, k=700), "pool8"),
+    ("k_eq_n_dense", _shape("cfg2", N=2048, k=2048), "planted"),
+    ("cfg4", synth.CONFIGS["cfg4"], "planted"),
+]
+
+
+@pytest.mark.parametrize("name,shape,variant", KVPAIR, ids=[s[0] for s in KVPAIR])
+def test_decode_parity_kv_pair(name, shape, variant):
+    """K and V rows of a token adjacent in HBM (the bench's cache layout): one
+    512-byte bulk copy gathers both; results must not change."""
+    case = synth.make_case(shape, seed=17, variant=variant)
+    g = gpu_step(case, shape.k, fused=True, kv_pair=True)
+    st = check_decode(case, g, shape.k, code_rows_sample=65536 if shape.N > 100000 else None)
+    print(name, st)
