@@ -119,7 +119,7 @@ DecodePlan plan_decode(int B, int Hq, int Hkv, int d, int rbits, int64_t n_max, 
   const int hs = dec_hist_stride(pl.nbins + 1);
   // workspace (every section 256-byte aligned)
   size_t off = 0;
-  pl.ws_sync = off;  off += M > 1 ? up256((size_t)units * 4 * 4) : 0;
+  pl.ws_sync = off;  off += up256((size_t)units * 4 * 4);          // [2] = threshold hint (any M)
   pl.ws_hist = off;  off += M > 1 ? up256((size_t)units * M * hs * 4) : 0;
   pl.ws_tot = off;   off += M > 1 ? up256((size_t)units * hs * 4) : 0;
   pl.ws_part = off;  off += M > 1 ? up256((size_t)units * M * dec_part_stride(GT, d) * 4) : 0;
@@ -138,7 +138,7 @@ cudaError_t launch_decode(DecodeParams& p, const DecodePlan& pl, void* ws, int i
   { static const int h = [] { const char* e = std::getenv("HATA_HINT"); return e ? std::atoi(e) : 1; }(); p.use_hint = h; }
   p.M = pl.M; p.stages = pl.stages; p.chunk = pl.chunk; p.nbins = pl.nbins; p.rows_cap = pl.rows_cap; p.R_cap = pl.R_cap;
   p.d_smem = pl.d_smem;
-  p.ws_sync = pl.M > 1 ? reinterpret_cast<unsigned*>(w + pl.ws_sync) : nullptr;
+  p.ws_sync = reinterpret_cast<unsigned*>(w + pl.ws_sync);
   p.ws_hist = pl.M > 1 ? reinterpret_cast<int32_t*>(w + pl.ws_hist) : nullptr;
   p.ws_part = pl.M > 1 ? reinterpret_cast<float*>(w + pl.ws_part) : nullptr;
   p.ws_tot = pl.M > 1 ? reinterpret_cast<int32_t*>(w + pl.ws_tot) : nullptr;

@@ -29,7 +29,7 @@ constexpr int DEC_STAGE_BYTES = 32768;       // one bulk copy of codes (few larg
 constexpr int DEC_MAX_STAGES = 4;            // code ring depth (up to 128 KB in flight)
 constexpr int DEC_D_SMEM_MAX = 16384;        // tokens/CTA whose D (u16) stays in smem
 constexpr int DEC_CHUNK_ALIGN = 64;          // tokens
-constexpr int DEC_BC_WPT = 2;               // candidate-bitmap words per thread (fast selection path)
+constexpr int DEC_BC_WPT = 4;               // candidate-bitmap words per thread (fast selection path)
 constexpr int DEC_HINT_SLACK = 2;           // hint threshold slack (bins)
 constexpr int DEC_WIN = 8;                  // bins [Th - 6, Th + 1] of every rank's prefix counts read with the totals
 constexpr int DEC_MAX_RANKS = 32;            // M cap (histogram exchange is M x nbins per rank)
@@ -70,7 +70,7 @@ struct DecodeParams {
   int32_t* ws_tot;         // [units, hs] sum over the ranks of cum_r (atomics)        (M > 1)
   uint16_t* ws_D;          // [units, M, chunk] D when it does not fit in smem (!d_smem)
   float* ws_part;          // [units, M, GT, d+2]          (M > 1)
-  unsigned* ws_sync;       // [units, 4]: barrier, done, threshold hint, -   (M > 1)
+  unsigned* ws_sync;       // [units, 4]: barrier, done (M > 1), threshold hint, -
   // sequence-shard phase 1 (hata_shard_candidates): stop after the select and
   // emit (D, global index) candidates instead of attending.
   int cand_mode;

@@ -12,6 +12,7 @@
 //   4  gather-fused softmax attention over that share Alg. 3 lines 14-17
 //   5  rank-ordered flash-decoding merge by the last rank to finish
 #pragma once
+#include <type_traits>
 #include "hata_attn_mma.cuh"
 #include "hata_decode.cuh"
 
@@ -197,9 +198,9 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
     // q and the new key/value first (they gate the q-hash), then the code
     // chunk in a few large copies: a CTA's TMA requests are served in order
     const uint32_t qbytes = (uint32_t)(G * D_HEAD * EB), kbytes = append ? (uint32_t)(D_HEAD * EB) : 0u;
-    mbar_arrive_expect_tx(&bars[NST + 1], qbytes + 2 * kbytes + (M > 1 ? 16u : 0u));
+    mbar_arrive_expect_tx(&bars[NST + 1], qbytes + 2 * kbytes + (p.ws_sync ? 16u : 0u));
     bulk_g2s(qraw, qg, qbytes, &bars[NST + 1]);
-    if (M > 1) bulk_g2s(misc + 12, p.ws_sync + 4 * u, 16u, &bars[NST + 1]);   // [14] = threshold hint
+    if (p.ws_sync) bulk_g2s(misc + 12, p.ws_sync + 4 * u, 16u, &bars[NST + 1]);   // [14] = threshold hint
     if (kbytes) {                                                   // new key and value rows
       bulk_g2s(qraw + G * D_HEAD, reinterpret_cast<const T*>(p.k_new) + (int64_t)u * D_HEAD, kbytes, &bars[NST + 1]);
       bulk_g2s(qraw + (G + 1) * D_HEAD, reinterpret_cast<const T*>(p.v_new) + (int64_t)u * D_HEAD, kbytes, &bars[NST + 1]);
@@ -215,7 +216,7 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
   uint32_t* Bc = reinterpret_cast<uint32_t*>(smem + L.bc);
   const int nbw = p.d_smem ? dec_dchunk(p.chunk) / 32 : 0;          // bitmap words
   int Th = -1;
-  const bool hinted = p.use_hint && M > 1 && nbw > 0 && nbw <= DEC_BC_WPT * DEC_THREADS;
+  const bool hinted = p.use_hint && p.ws_sync && nbw > 0 && nbw <= DEC_BC_WPT * DEC_THREADS;
   const int kp = (int)(n < (int64_t)p.k ? n : (int64_t)p.k);      // k' = min(k, n)  (R10)
   auto chunk_len = [&](int rr) -> int {                            // valid tokens of rank rr
     const int64_t a = (int64_t)rr * per, z = min((int64_t)n, a + per);
@@ -494,6 +495,26 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
     int total;
     cum = block_excl_scan(mysum, misc + 16, total);                  // #{local D < i0}
   }
+  auto build_bitmap = [&]() {
+    if (Th < 0) return;
+    // candidate bitmap (M > 1: while the other ranks arrive): thread t owns
+    // words [t*WPT, (t+1)*WPT) (32 tokens each); bit i of word w = (D[32w+i] <= Th)
+    const uint32_t th_k = (uint32_t)Th * 0x10001u + 0x80008000u;
+    const int WPT = (nbw + DEC_THREADS - 1) / DEC_THREADS;
+    for (int w = tid * WPT; w < min(nbw, (tid + 1) * WPT); ++w) {
+      const uint4* dq = reinterpret_cast<const uint4*>(Dloc + 32 * w);
+      uint32_t m = 0u;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const uint4 x = dq[c];
+        const uint32_t a0 = (th_k - x.x) & 0x80008000u, a1 = (th_k - x.y) & 0x80008000u;
+        const uint32_t a2 = (th_k - x.z) & 0x80008000u, a3 = (th_k - x.w) & 0x80008000u;
+        m |= (((a0 >> 15) & 1u) | ((a0 >> 30) & 2u) | ((a1 >> 13) & 4u) | ((a1 >> 28) & 8u) |
+              ((a2 >> 11) & 16u) | ((a2 >> 26) & 32u) | ((a3 >> 9) & 64u) | ((a3 >> 24) & 128u)) << (8 * c);
+      }
+      Bc[w] = m;
+    }
+  };
   if (tid == 0) { misc[0] = -1; misc[1] = 0; misc[4] = p.nbins; }
   if (M > 1) {
     int32_t* gc = p.ws_hist + ((int64_t)u * M + r) * hs;
@@ -510,25 +531,7 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
     }
     __syncthreads();
     if (tid == 0) red_add_release_gpu(sync, 1u);   // release the CTA's writes (cumulative over bar.sync)
-    if (Th >= 0) {
-      // candidate bitmap while the other ranks arrive: thread t owns words
-      // [t*WPT, (t+1)*WPT) (32 tokens each); bit i of word w = (D[32w+i] <= Th)
-      const uint32_t th_k = (uint32_t)Th * 0x10001u + 0x80008000u;
-      const int WPT = (nbw + DEC_THREADS - 1) / DEC_THREADS;
-      for (int w = tid * WPT; w < min(nbw, (tid + 1) * WPT); ++w) {
-        const uint4* dq = reinterpret_cast<const uint4*>(Dloc + 32 * w);
-        uint32_t m = 0u;
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          const uint4 x = dq[c];
-          const uint32_t a0 = (th_k - x.x) & 0x80008000u, a1 = (th_k - x.y) & 0x80008000u;
-          const uint32_t a2 = (th_k - x.z) & 0x80008000u, a3 = (th_k - x.w) & 0x80008000u;
-          m |= (((a0 >> 15) & 1u) | ((a0 >> 30) & 2u) | ((a1 >> 13) & 4u) | ((a1 >> 28) & 8u) |
-                ((a2 >> 11) & 16u) | ((a2 >> 26) & 32u) | ((a3 >> 9) & 64u) | ((a3 >> 24) & 128u)) << (8 * c);
-        }
-        Bc[w] = m;
-      }
-    }
+    build_bitmap();
     HATA_TRACE(27);
     if (tid == 0) {
       for (unsigned spins = 0; ld_acquire_gpu(sync) < (unsigned)M;)
@@ -558,6 +561,7 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
     }
     if (wl) win[tid] = wv;
   } else {
+    build_bitmap();
     HATA_TRACE(3);
     int c = cum;
 #pragma unroll
@@ -569,7 +573,7 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
   __syncthreads();
   const int thr = misc[0];
   const int need = misc[1];
-  if (M > 1 && r == 0 && tid == 0) reinterpret_cast<int*>(p.ws_sync)[4 * u + 2] = thr;   // next launch's hint
+  if (p.ws_sync && r == 0 && tid == 0) reinterpret_cast<int*>(p.ws_sync)[4 * u + 2] = thr;   // next launch's hint
   // this rank's tie quota and the selection position of its first token
   // (computed by every warp: no further barrier); the loads are issued here
   // and consumed after the counting pass below
@@ -621,7 +625,7 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
     if (M > 1 && thr >= 0) {
       ti -= bl;
       int incl = ti;
-  #pragma unroll
+#pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
         const int v = __shfl_up_sync(0xffffffffu, incl, o);
         if (lane >= o) incl += v;
@@ -629,7 +633,7 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
       const int qv = max(0, min(need - (incl - ti), ti));
       const int sel = bl + qv;
       int inc2 = sel;
-  #pragma unroll
+#pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
         const int v = __shfl_up_sync(0xffffffffu, inc2, o);
         if (lane >= o) inc2 += v;
@@ -646,49 +650,56 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
   const bool fast = Th >= 0 && thr >= 0 && thr <= Th;
   if (fast) {
     const int WPT = (nbw + DEC_THREADS - 1) / DEC_THREADS;
-    uint32_t ltw[DEC_BC_WPT], eqw[DEC_BC_WPT];
-    int nlt = 0, neq = 0;
+    // WPTC: compile-time bound on the words per thread (1 for chunks of up
+    // to 8K tokens, the common multi-rank case; DEC_BC_WPT otherwise)
+    auto fast_select = [&](auto wptc) {
+      constexpr int WPTC = decltype(wptc)::value;
+      uint32_t ltw[WPTC], eqw[WPTC];
+      int nlt = 0, neq = 0;
 #pragma unroll
-    for (int j = 0; j < DEC_BC_WPT; ++j) {
-      const int w = tid * WPT + j;
-      uint32_t lt = 0u, eq = 0u;
-      if (j < WPT && w < nbw && Bc[w]) {
-        // the word's 32 distances by SWAR (bounded cost for dense words)
-        const uint4* dq = reinterpret_cast<const uint4*>(Dloc + 32 * w);
+      for (int j = 0; j < WPTC; ++j) {
+        const int w = tid * WPT + j;
+        uint32_t lt = 0u, eq = 0u;
+        if (j < WPT && w < nbw && Bc[w]) {
+          // the word's 32 distances by SWAR (bounded cost for dense words)
+          const uint4* dq = reinterpret_cast<const uint4*>(Dloc + 32 * w);
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          const uint4 x = dq[c];
-          uint32_t l4[4], e4[4];
-          swar(x.x, l4[0], e4[0]); swar(x.y, l4[1], e4[1]); swar(x.z, l4[2], e4[2]); swar(x.w, l4[3], e4[3]);
-          lt |= pack8(l4) << (8 * c);
-          eq |= pack8(e4) << (8 * c);
+          for (int c = 0; c < 4; ++c) {
+            const uint4 x = dq[c];
+            uint32_t l4[4], e4[4];
+            swar(x.x, l4[0], e4[0]); swar(x.y, l4[1], e4[1]); swar(x.z, l4[2], e4[2]); swar(x.w, l4[3], e4[3]);
+            lt |= pack8(l4) << (8 * c);
+            eq |= pack8(e4) << (8 * c);
+          }
+        }
+        ltw[j] = lt;
+        eqw[j] = eq;
+        nlt += __popc(lt);
+        neq += __popc(eq);
+      }
+      int ti_b, lt_tot, ti_tot;
+      int lt_b = block_excl_scan2(nlt, neq, misc + 16, ti_b, lt_tot, ti_tot);
+      compute_quota();
+      Rr = lt_tot + min(ti_tot, quota);
+#pragma unroll
+      for (int j = 0; j < WPTC; ++j) {
+        const int w = tid * WPT + j;
+        if (j < WPT && w < nbw && (ltw[j] | eqw[j])) {
+          // the first max(0, quota - ti_b) ties of the word are taken (R8)
+          uint32_t ties = 0u, e = eqw[j];
+          for (int take = min(__popc(e), max(quota - ti_b, 0)); take > 0; --take) {
+            ties |= e & (0u - e);
+            e &= e - 1u;
+          }
+          int pl = lt_b + min(ti_b, quota);
+          for (uint32_t sel = ltw[j] | ties; sel; sel &= sel - 1u) rows[pl++] = (int32_t)t0 + 32 * w + (__ffs(sel) - 1);
+          lt_b += __popc(ltw[j]);
+          ti_b += __popc(eqw[j]);
         }
       }
-      ltw[j] = lt;
-      eqw[j] = eq;
-      nlt += __popc(lt);
-      neq += __popc(eq);
-    }
-    int ti_b, lt_tot, ti_tot;
-    int lt_b = block_excl_scan2(nlt, neq, misc + 16, ti_b, lt_tot, ti_tot);
-    compute_quota();
-    Rr = lt_tot + min(ti_tot, quota);
-#pragma unroll
-    for (int j = 0; j < DEC_BC_WPT; ++j) {
-      const int w = tid * WPT + j;
-      if (j < WPT && w < nbw && (ltw[j] | eqw[j])) {
-        // the first max(0, quota - ti_b) ties of the word are taken (R8)
-        uint32_t ties = 0u, e = eqw[j];
-        for (int take = min(__popc(e), max(quota - ti_b, 0)); take > 0; --take) {
-          ties |= e & (0u - e);
-          e &= e - 1u;
-        }
-        int pl = lt_b + min(ti_b, quota);
-        for (uint32_t sel = ltw[j] | ties; sel; sel &= sel - 1u) rows[pl++] = (int32_t)t0 + 32 * w + (__ffs(sel) - 1);
-        lt_b += __popc(ltw[j]);
-        ti_b += __popc(eqw[j]);
-      }
-    }
+    };
+    if (WPT == 1) fast_select(std::integral_constant<int, 1>{});
+    else fast_select(std::integral_constant<int, DEC_BC_WPT>{});
   } else {
     int lt_m = 0, eq_m = 0;
     if (thr >= 0) {
@@ -704,7 +715,7 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
     HATA_CLK(1);
     // warp-inclusive scans of both counts
     int lt_i = lt_m, eq_i = eq_m;
-  #pragma unroll
+#pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const int a = __shfl_up_sync(0xffffffffu, lt_i, o), e = __shfl_up_sync(0xffffffffu, eq_i, o);
       if (lane >= o) { lt_i += a; eq_i += e; }
@@ -719,7 +730,7 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
     HATA_CLK(4);
     // this thread's exclusive offsets within the rank, and the rank totals
     int lt_b = lt_i - lt_m, ti_b = eq_i - eq_m, lt_tot = 0, ti_tot = 0;
-  #pragma unroll
+#pragma unroll
     for (int w = 0; w < DEC_WARPS; ++w) {
       const int cl = wcnt[2 * w], ct = wcnt[2 * w + 1];
       if (w < warp) { lt_b += cl; ti_b += ct; }
@@ -749,7 +760,7 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
           auto emit = [&](int pl, int i) { rows[pl] = (int32_t)t0 + (tid * S8 + c) * 8 + i; };
           if (__popc(sel8) >= 3) {                                     // dense block (e.g. a recent window):
             int rr = 0;                                                // predicated, no per-pick popc
-  #pragma unroll
+#pragma unroll
             for (int i = 0; i < 8; ++i)
               if ((sel8 >> i) & 1u) emit(base + rr++, i);
           } else {

@@ -97,6 +97,9 @@ HINTED = [
     ("tie_pool8", _shape("cfg2", N=9000, k=700), "pool8"),
     ("tie_dup", _shape("cfg2", N=8192, k=333), "dup"),
     ("cfg2", synth.CONFIGS["cfg2"], "planted"),
+    ("m1_b16", _shape("cfg3", N=4096, k=200), "planted"),          # one rank per unit (no exchange)
+    ("m1_b16_pool8", _shape("cfg3", N=4096, k=300), "pool8"),
+    ("m2_g5_r256_32k", _shape("cfg5", B=8, N=65536, k=1024), "planted"),   # CFG-5 layer: 2 ranks, 32K-token chunks
 ]
 
 
@@ -114,10 +117,11 @@ def test_decode_parity_hinted(name, shape, variant):
 
 @pytest.mark.parametrize("first,second", [("planted", "pool8"), ("pool8", "planted"), ("planted", "dup"),
                                           ("dup", "planted"), ("equal", "planted"), ("planted", "equal")])
-def test_decode_parity_stale_hint(first, second):
+@pytest.mark.parametrize("B", [1, 16], ids=["ranks", "one_rank"])
+def test_decode_parity_stale_hint(first, second, B):
     """The hint comes from a different problem (higher or lower threshold):
     the selection falls back or scans extra candidates, never changes."""
-    shape = _shape("cfg2", N=12000, k=600)
+    shape = _shape("cfg2", B=B, N=12000 if B == 1 else 3000, k=600 if B == 1 else 150)
     ws = _ws_for(shape, shape.k)
     a = synth.make_case(shape, seed=21, variant=first)
     gpu_step(a, shape.k, fused=True, workspace=ws)
