@@ -122,8 +122,15 @@ hata_status hata_append(const void* k_new, const void* v_new, hata_dtype dt, con
  *   workspace  device scratch of >= hata_decode_workspace_size(...) bytes,
  *              256-byte aligned, ZERO-FILLED before its first use (every
  *              launch leaves its synchronisation words zeroed again); one
- *              workspace per concurrently running call.  May be NULL when
- *              the size is 0.
+ *              workspace per concurrently running call.  It also keeps each
+ *              (b, KV head)'s last selection threshold, a hint that lets the
+ *              next launch visit only candidate tokens -- it changes the
+ *              work, never the result; keep one workspace per attention
+ *              layer to keep the hint per layer.  May be NULL when the size
+ *              is 0.
+ * Launched with programmatic dependent launch: the kernel reads W before
+ * griddepcontrol.wait and everything else (q, k_new, v_new, n, codes, K/V,
+ * workspace) after it.
  * One cooperative kernel launch of M x (B*H_kv) CTAs (hata_decode_ranks()).
  * Errors: INVALID_ARG (k < 1, H_q % H_kv, rbits % 32, n_max < 0, nulls),
  *         UNSUPPORTED, WORKSPACE, CUDA.  n[b] == 0 yields zero output and
