@@ -20,7 +20,8 @@ __device__ __forceinline__ void attend_rows_mma(const int32_t* rows, int Rr, con
                                                 const __nv_bfloat16* __restrict__ Vb, int64_t kv_st, const __nv_bfloat16* qb,
                                                 int G, float scale, uint8_t* kvbuf, int rows_cap, int rowb,
                                                 float* m_s, float* l_s, AttnState<GT, D_HEAD>& st,
-                                                uint64_t* bar, int kvpair, unsigned long long* tr = nullptr, int tb = 16) {
+                                                uint64_t* bar, uint64_t* bar2, int kvpair, unsigned long long* tr = nullptr,
+                                                int tb = 16) {
   static_assert(GT <= 8, "heads per group <= 8");
   constexpr int CH = D_HEAD * 2 / 16;            // 16-byte chunks per row
   constexpr int KS = D_HEAD / 16;                // k-steps over the head dim
@@ -34,6 +35,8 @@ __device__ __forceinline__ void attend_rows_mma(const int32_t* rows, int Rr, con
   if (kvpair) rowb = 2 * D_HEAD * 2 + DEC_ROW_PAD;
   uint8_t* Ks = kvbuf;
   uint8_t* Vs = kvpair ? kvbuf + D_HEAD * 2 : kvbuf + rows_cap * rowb;
+  uint8_t* const Ks0 = Ks;
+  uint8_t* const Vs0 = Vs;
 
   // Q as A fragments held in registers for the whole call, read once from the
   // bf16 rows as stored (qb: [G][D_HEAD] smem); heads >= G and rows 8..15 are zero
@@ -50,32 +53,45 @@ __device__ __forceinline__ void attend_rows_mma(const int32_t* rows, int Rr, con
   float m_run = -INFINITY, l_run = 0.f;          // head gid, this warp
   bool active = false;
 
-  uint32_t bpar = 0;
-  for (int r0 = 0; r0 < Rr; r0 += rows_cap) {
-    const int nb = min(rows_cap, Rr - r0);
-    __syncthreads();                             // previous batch fully consumed
-    // gather: one bulk copy per selected K or V row (TMA engine, no per-16B
-    // requests in the LSU), all on one mbarrier
-    constexpr uint32_t ROWBYTES = D_HEAD * 2;
-    if (tid == 0) mbar_arrive_expect_tx(bar, 2u * ROWBYTES * (uint32_t)nb);
+  // more rows than one staging area holds: two half-size buffers, the next
+  // batch's gather in flight while the current one is on the tensor cores
+  const bool dbl = Rr > rows_cap;
+  const int rc = dbl ? rows_cap / 2 : rows_cap;                   // rows per batch
+  constexpr uint32_t ROWBYTES = D_HEAD * 2;
+  auto issue = [&](int r0, int j) {
+    const int nb = min(rc, Rr - r0);
+    uint8_t* Kj = Ks + j * rc * rowb;
+    uint8_t* Vj = Vs + j * rc * rowb;
+    if (tid == 0) mbar_arrive_expect_tx((j ? bar2 : bar), 2u * ROWBYTES * (uint32_t)nb);
     __syncthreads();
-    if (r0 == 0) HATA_TRACE_AT(tr, tb + 4);
-    // request i -> warp i % NW, lane i / NW: a warp issues its bulk copies one
-    // lane after another, so spread them over all warps
+    // gather: one bulk copy per selected row (TMA engine, no per-16B requests
+    // in the LSU); request i -> warp i % NW, lane i / NW: a warp issues its
+    // bulk copies one lane after another, so spread them over all warps
     if (kvpair) {
       for (int i = lane * DEC_WARPS + warp; i < nb; i += DEC_THREADS)
-        bulk_g2s(Ks + i * rowb, Kb + (int64_t)rows[r0 + i] * kv_st, 2 * ROWBYTES, bar);
+        bulk_g2s(Kj + i * rowb, Kb + (int64_t)rows[r0 + i] * kv_st, 2 * ROWBYTES, (j ? bar2 : bar));
     } else {
       for (int i = lane * DEC_WARPS + warp; i < 2 * nb; i += DEC_THREADS) {
         const int which = i >= nb, rr = i - (which ? nb : 0);
         const __nv_bfloat16* src = (which ? Vb : Kb) + (int64_t)rows[r0 + rr] * kv_st;
-        bulk_g2s((which ? Vs : Ks) + rr * rowb, src, ROWBYTES, bar);
+        bulk_g2s((which ? Vj : Kj) + rr * rowb, src, ROWBYTES, (j ? bar2 : bar));
       }
     }
-    if (r0 == 0) HATA_TRACE_AT(tr, tb + 3);
-    mbar_wait(bar, bpar);
-    bpar ^= 1u;
+  };
+  uint32_t bpar = 0;                              // phase bit per buffer
+  __syncthreads();                                // the staging area is free
+  HATA_TRACE_AT(tr, tb + 4);
+  if (Rr > 0) issue(0, 0);
+  HATA_TRACE_AT(tr, tb + 3);
+  for (int r0 = 0, bi = 0; r0 < Rr; r0 += rc, ++bi) {
+    const int j = bi & 1;
+    const int nb = min(rc, Rr - r0);
+    if (dbl && r0 + rc < Rr) issue(r0 + rc, j ^ 1);              // its buffer was consumed last iteration
+    mbar_wait(j ? bar2 : bar, (bpar >> j) & 1u);
+    bpar ^= 1u << j;
     if (r0 == 0) HATA_TRACE_AT(tr, tb);
+    const uint8_t* Ks = Ks0 + j * rc * rowb;
+    const uint8_t* Vs = Vs0 + j * rc * rowb;
     for (int g0 = warp * 16; g0 < nb; g0 += DEC_WARPS * 16) {
       active = true;
       // S = Q K^T for rows g0 .. g0+15 (two 8-row tiles)

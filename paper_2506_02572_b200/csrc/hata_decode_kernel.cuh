@@ -797,7 +797,7 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
     const T* Vb = reinterpret_cast<const T*>(p.V) + (int64_t)b * p.kv_sb + (int64_t)g * p.kv_sh;
     if constexpr (EB == 2) {
       attend_rows_mma<GT, D_HEAD>(rows, Rr, Kb, Vb, p.kv_st, reinterpret_cast<const __nv_bfloat16*>(qraw), G, p.scale, smem + L.kv, p.rows_cap, L.rb,
-                                  m_s, l_s, st, &bars[NST + 3],
+                                  m_s, l_s, st, &bars[NST + 3], &bars[NST + 2],
                                   reinterpret_cast<const uint8_t*>(p.V) == reinterpret_cast<const uint8_t*>(p.K) + D_HEAD * EB &&
                                       p.kv_st == 2 * D_HEAD,
                                   p.trace);
