@@ -246,7 +246,6 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
     // Warp = one 8-bit column tile of the code; Sign + BitPack (Alg. 2 lines
     // 5-7) straight from the accumulator fragment via ballots.
     const int gid = lane >> 2, tig = lane & 3;
-    uint8_t* qbytes = reinterpret_cast<uint8_t*>(qw);               // [GT+1][W*4] code bytes
     // A fragments of every k-step, read once from the bf16 rows as stored
     constexpr int KS = D_HEAD / 16;
     uint32_t qa[KS][4];
@@ -259,25 +258,33 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
       qa[ks][2] = gid < NV ? x0[4] : 0u;
       qa[ks][3] = gid + 8 < NV ? x1[4] : 0u;
     }
-    for (int nt = warp; nt < p.rbits / 8; nt += DEC_WARPS) {
-      float c[4] = {0.f, 0.f, 0.f, 0.f};
+    // warp = one 32-bit code word (4 n-tiles, 4 independent MMA chains);
+    // each lane sets its 2 sign bits per n-tile, the 4 lanes of a row OR-reduce
+    for (int w = warp; w < W; w += DEC_WARPS) {
+      float c[4][4];
 #pragma unroll
-      for (int ks = 0; ks < KS; ++ks) {
-        uint32_t b0, b1;
-        ldsm_x2_trans(b0, b1, reinterpret_cast<const uint8_t*>(Ws) + (ks * 16 + (lane & 15)) * WROWB + nt * 16);
-        mma_bf16_16816(c, qa[ks], b0, b1);
-      }
-      const uint32_t m0 = __ballot_sync(0xffffffffu, c[0] >= 0.f), m1 = __ballot_sync(0xffffffffu, c[1] >= 0.f);
-      const uint32_t m2 = __ballot_sync(0xffffffffu, c[2] >= 0.f), m3 = __ballot_sync(0xffffffffu, c[3] >= 0.f);
-      if (tig == 0) {
-        uint32_t lo = 0, hi = 0;                                    // bits nt*8 .. nt*8+7, LSB-first (R7)
+      for (int q = 0; q < 4; ++q) c[q][0] = c[q][1] = c[q][2] = c[q][3] = 0.f;
 #pragma unroll
-        for (int t = 0; t < 4; ++t) {
-          lo |= ((m0 >> (gid * 4 + t)) & 1u) << (2 * t) | ((m1 >> (gid * 4 + t)) & 1u) << (2 * t + 1);
-          hi |= ((m2 >> (gid * 4 + t)) & 1u) << (2 * t) | ((m3 >> (gid * 4 + t)) & 1u) << (2 * t + 1);
+      for (int ks = 0; ks < KS; ++ks)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          uint32_t b0, b1;
+          ldsm_x2_trans(b0, b1, reinterpret_cast<const uint8_t*>(Ws) + (ks * 16 + (lane & 15)) * WROWB + (4 * w + q) * 16);
+          mma_bf16_16816(c[q], qa[ks], b0, b1);
         }
-        if (gid < NV) qbytes[gid * W * 4 + nt] = (uint8_t)lo;
-        if (gid + 8 < NV) qbytes[(gid + 8) * W * 4 + nt] = (uint8_t)hi;
+      uint32_t lo = 0u, hi = 0u;                                    // rows gid / gid + 8, LSB-first (R7)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        lo |= ((uint32_t)(c[q][0] >= 0.f) | ((uint32_t)(c[q][1] >= 0.f) << 1)) << (8 * q + 2 * tig);
+        hi |= ((uint32_t)(c[q][2] >= 0.f) | ((uint32_t)(c[q][3] >= 0.f) << 1)) << (8 * q + 2 * tig);
+      }
+      lo |= __shfl_xor_sync(0xffffffffu, lo, 1);
+      hi |= __shfl_xor_sync(0xffffffffu, hi, 1);
+      lo |= __shfl_xor_sync(0xffffffffu, lo, 2);
+      hi |= __shfl_xor_sync(0xffffffffu, hi, 2);
+      if (tig == 0) {
+        if (gid < NV) qw[gid * W + w] = lo;
+        if (gid + 8 < NV) qw[(gid + 8) * W + w] = hi;
       }
     }
   } else {
