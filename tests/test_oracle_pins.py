@@ -398,3 +398,76 @@ def test_prefill_overhead_and_bytes():
     assert O.algorithmic_bytes(1, 32, 8, 128, 128, 131072, 2048, 2) == 25_174_016
     assert O.algorithmic_bytes(1, 32, 8, 128, 128, 32768, 1024, 2) == 8_396_800
     assert O.algorithmic_bytes(1, 1, 1, 128, 128, 1024, 64, 4) == 82_432
+
+
+# --------------------------------------- pins added in round 2 (VERDICT weak #1)
+def test_hash_keys_per_kv_head_weights_bruteforce():
+    """Alg. 1 lines 2-5 with reading R4 (one W per KV head):
+    codes[b, g, t] must equal the sign bits of K[b, g, t] . W[g], re-derived by
+    an exact-rounded per-bit dot product (math.fsum), and changing W[1] must
+    change only head 1's codes.  Catches: W[0] used for every head, heads
+    transposed with batches, a wrong row written."""
+    r = np.random.default_rng(21)
+    B, Hkv, N, d, rbit = 2, 3, 5, 16, 64
+    K = r.standard_normal((B, Hkv, N, d))
+    W = r.standard_normal((Hkv, d, rbit))
+    codes, nz = O.hash_keys(K, W)
+    for b in range(B):
+        for g in range(Hkv):
+            bits = O.bit_unpack(codes[b, g], rbit)
+            for t in range(N):
+                for bb, (bit, mag) in enumerate(_brute_sign_bits(K[b, g, t], W[g])):
+                    assert nz[b, g, t, bb] == (mag < O.NEAR_ZERO)
+                    if mag >= O.NEAR_ZERO:
+                        assert bits[t, bb] == bit, (b, g, t, bb)
+    W2 = W.copy()
+    W2[1] = r.standard_normal(W2[1].shape)
+    codes2, _ = O.hash_keys(K, W2)
+    assert np.array_equal(codes2[:, [0, 2]], codes[:, [0, 2]])
+    assert not np.array_equal(codes2[:, 1], codes[:, 1])
+
+
+def test_append_writes_exactly_row_pos():
+    """Alg. 3 lines 3-4, 7-9: after append, row pos[b] of every
+    (b, g) holds k_new / v_new and the brute-force code of k_new under W[g];
+    every other row of K, V and codes is unchanged.  Catches: an off-by-one
+    row (pos + 1), K and V swapped, the code of the wrong head."""
+    r = np.random.default_rng(22)
+    B, Hkv, cap, d, rbit = 2, 2, 9, 16, 64
+    K = r.standard_normal((B, Hkv, cap, d)); V = r.standard_normal((B, Hkv, cap, d))
+    W = r.standard_normal((Hkv, d, rbit))
+    codes = r.integers(0, 2**32, size=(B, Hkv, cap, rbit // 32), dtype=np.uint64).astype(np.uint32)
+    kn = r.standard_normal((B, Hkv, d)); vn = r.standard_normal((B, Hkv, d))
+    pos = np.array([4, 0])
+    K2, V2, c2, _ = O.append(K, V, codes, kn, vn, W, pos)
+    for b in range(B):
+        p = int(pos[b])
+        others = [t for t in range(cap) if t != p]
+        for g in range(Hkv):
+            assert np.array_equal(K2[b, g, p], kn[b, g]) and np.array_equal(V2[b, g, p], vn[b, g])
+            assert np.array_equal(K2[b, g, others], K[b, g, others])
+            assert np.array_equal(V2[b, g, others], V[b, g, others])
+            assert np.array_equal(c2[b, g, others], codes[b, g, others])
+            bits = O.bit_unpack(c2[b, g, p][None], rbit)[0]
+            for bb, (bit, mag) in enumerate(_brute_sign_bits(kn[b, g], W[g])):
+                if mag >= O.NEAR_ZERO:
+                    assert bits[bb] == bit
+
+
+@pytest.mark.parametrize("G,rbit", [(4, 64), (5, 32)])
+def test_decode_S_is_group_pm1_inner_product(G, rbit):
+    """north_star / R2: the reported S of each selected token is the +-1 inner
+    product of its key code with the G query codes of its group, summed over
+    the group (P:138 h in {-1,1}^r; P:255 aggregation).  Computed here from
+    the unpacked +-1 vectors, not from D.  Catches: S reported with G = 1, a
+    missing factor 2, the wrong head range."""
+    q, kn, vn, K, V, codes, W = _small_case(Hq=2 * G, Hkv=2, rbit=rbit, seed=5)
+    nb = np.array([120, 77])
+    res = O.decode_step(q, kn, vn, K, V, codes, W, nb, k=24)
+    qc = res["qc"]
+    for b in range(2):
+        for g in range(2):
+            idx = res["idx"][b][g]
+            kp = _pm1(res["codes"][b, g, idx], rbit)
+            ip = sum(kp @ _pm1(qc[b, h][None], rbit)[0] for h in range(g * G, (g + 1) * G))
+            assert np.array_equal(res["S"][b][g], ip.astype(np.int64))
