@@ -70,13 +70,16 @@ typedef struct CUstream_st* hata_stream_t; /* == cudaStream_t */
  *   K       [B, H_kv, cap, d] (strides ks), rows [t0, t0 + n) are hashed.
  *   W       [H_kv, d, rbits].
  *   codes   output rows [t0, t0 + n) of [B, H_kv, cap, rbits/32] (strides cs).
- * bf16 inputs run on the tcgen05 tensor cores (fp32 accumulation in TMEM,
- * sign-pack epilogue); fp32 inputs run on CUDA cores (fp32 FMA).
+ *   cap     rows allocated per (b, KV head) in K and codes; t0 + n > cap ->
+ *           CAPACITY (nothing enqueued).
+ * bf16 inputs run on the tensor cores (mma.sync m16n8k16 HMMA, exact bf16
+ * products, fp32 accumulation, sign-pack epilogue); fp32 inputs run on CUDA
+ * cores (fp32 FMA).
  * Errors: INVALID_ARG (null pointers, n < 0, rbits % 32, strides),
- *         UNSUPPORTED (d, rbits, dtype), CUDA.
+ *         CAPACITY, UNSUPPORTED (d, rbits, dtype), CUDA.
  * ------------------------------------------------------------------------ */
 hata_status hata_hash_keys(const void* K, hata_strides ks, hata_dtype dt, const void* W, int B, int H_kv, int d,
-                           int rbits, int64_t t0, int64_t n, uint32_t* codes, hata_strides cs,
+                           int rbits, int64_t t0, int64_t n, int64_t cap, uint32_t* codes, hata_strides cs,
                            hata_stream_t stream);
 
 /* ------------------------------------------------------------------------
@@ -111,7 +114,9 @@ hata_status hata_append(const void* k_new, const void* v_new, hata_dtype dt, con
  *   q          [B, H_q, d] dtype dt.
  *   K, V       caches (strides kvs), dtype dt.  codes (strides cs).  W as above.
  *   n          DEVICE int64 [B]: tokens per sequence incl. the appended one.
- *   n_max      host upper bound on n[b] (sizes the launch and the workspace).
+ *   n_max      host upper bound on n[b] (sizes the launch and the workspace);
+ *              a device n[b] > n_max is treated as n_max (cannot be validated
+ *              synchronously).
  *   k          token budget per (b, KV head), >= 1; k > n[b] clamps (R10).
  *   scale      softmax scale; 0 selects 1/sqrt(d) (R12).
  *   out        [B, H_q, d] dtype out_dt (fp32 recommended for parity, R14).
@@ -122,7 +127,9 @@ hata_status hata_append(const void* k_new, const void* v_new, hata_dtype dt, con
  *   workspace  device scratch of >= hata_decode_workspace_size(...) bytes,
  *              256-byte aligned, ZERO-FILLED before its first use (every
  *              launch leaves its synchronisation words zeroed again); one
- *              workspace per concurrently running call.  It also keeps each
+ *              workspace per concurrently running call.  A workspace is tied
+ *              to (B, H_kv, G*rbits): launches on it may change n_max and k
+ *              (its size must cover the largest), not those three.  It also keeps each
  *              (b, KV head)'s last selection threshold, a hint that lets the
  *              next launch visit only candidate tokens -- it changes the
  *              work, never the result; keep one workspace per attention
@@ -150,7 +157,8 @@ hata_status hata_decode_topk_attn(const void* q, const void* K, const void* V, h
  *                and value; written with HashEncode(k_new) at row n[b]-1 of
  *                K, V and codes, then scored like every cached token (R11).
  *   n            DEVICE int64 [B]: tokens per sequence INCLUDING the new one.
- *   cap          rows allocated per (b, KV head); n_max > cap -> CAPACITY.
+ *   cap          rows allocated per (b, KV head); n_max > cap -> CAPACITY; a
+ *                device row n[b]-1 >= cap is not written.
  * Every other argument as for hata_decode_topk_attn; the result equals
  * hata_append followed by hata_decode_topk_attn.
  * ------------------------------------------------------------------------ */
@@ -213,6 +221,21 @@ hata_status hata_shard_partial_attn(const void* q, const void* K, const void* V,
  * out = sum acc_r e^{m_r - M} / L. */
 hata_status hata_shard_combine(const float* partials, int P, int B, int H_q, int d, void* out, hata_dtype out_dt,
                                hata_stream_t stream);
+
+/* ------------------------------------------------------------------------
+ * Process-wide options of the decode launches (default: all on).
+ *   HATA_OPT_SELECTION_HINT  1: use the previous launch's threshold kept in the
+ *                            workspace to visit only candidate tokens in the
+ *                            select (changes the work, never the result);
+ *                            0: always run the full selection scan.
+ *   HATA_OPT_PDL             1: launch with programmatic dependent launch (the
+ *                            prologue overlaps the preceding kernel); 0: plain
+ *                            stream order.
+ * Returns INVALID_ARG for an unknown option.  Thread safe; affects launches
+ * enqueued after the call.
+ * ------------------------------------------------------------------------ */
+typedef enum { HATA_OPT_SELECTION_HINT = 0, HATA_OPT_PDL = 1 } hata_option;
+hata_status hata_set_option(hata_option opt, int value);
 
 /* ------------------------------------------------------------------------ */
 const char* hata_status_string(hata_status s);

@@ -18,7 +18,7 @@ import torch
 from . import _lib
 from ._lib import HataError, Strides  # noqa: F401
 
-__all__ = ["hash_keys", "append", "decode_topk_attn", "decode_step", "decode_workspace_size", "decode_ranks",
+__all__ = ["set_option", "hash_keys", "append", "decode_topk_attn", "decode_step", "decode_workspace_size", "decode_ranks",
            "shard_candidates", "shard_select", "shard_partial_attn", "shard_combine", "HataError", "lib"]
 
 
@@ -60,13 +60,19 @@ def _need_cuda(*ts):
             raise HataError("all tensors must be CUDA tensors (no CPU path)")
 
 
+def set_option(name: str, value: int):
+    """hata_set_option: "selection_hint" or "pdl" (process-wide, default on)."""
+    opt = {"selection_hint": _lib.HATA_OPT_SELECTION_HINT, "pdl": _lib.HATA_OPT_PDL}[name]
+    _lib.check(lib().hata_set_option(opt, int(value)), "hata_set_option")
+
+
 def hash_keys(K, W, codes, t0: int = 0, n: int | None = None, stream=None):
     """Alg. 1 lines 2-5: codes[:, :, t0:t0+n] = HashEncode(K[:, :, t0:t0+n]) (in place)."""
     _need_cuda(K, W, codes)
     B, Hkv, cap, d = K.shape
     rbits = W.shape[2]
     n = cap - t0 if n is None else n
-    _lib.check(lib().hata_hash_keys(_p(K), _strides4(K), _dt(K), _p(W.contiguous()), B, Hkv, d, rbits, t0, n,
+    _lib.check(lib().hata_hash_keys(_p(K), _strides4(K), _dt(K), _p(W.contiguous()), B, Hkv, d, rbits, t0, n, cap,
                                     _p(codes), _strides4(codes), _stream(stream)), "hata_hash_keys")
     return codes
 

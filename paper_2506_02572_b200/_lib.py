@@ -16,6 +16,8 @@ LIB_PATH = os.path.join(_HERE, os.environ.get("HATA_LIB", "libhata.so"))
 HATA_OK = 0
 HATA_F32 = 0
 HATA_BF16 = 1
+HATA_OPT_SELECTION_HINT = 0
+HATA_OPT_PDL = 1
 
 c_i32 = ctypes.c_int
 c_i64 = ctypes.c_int64
@@ -29,8 +31,8 @@ class Strides(ctypes.Structure):
 
 
 _SIGS = {
-    "hata_hash_keys": (c_i32, [c_ptr, Strides, c_i32, c_ptr, c_i32, c_i32, c_i32, c_i32, c_i64, c_i64, c_ptr,
-                               Strides, c_ptr]),
+    "hata_hash_keys": (c_i32, [c_ptr, Strides, c_i32, c_ptr, c_i32, c_i32, c_i32, c_i32, c_i64, c_i64, c_i64,
+                               c_ptr, Strides, c_ptr]),
     "hata_append": (c_i32, [c_ptr, c_ptr, c_i32, c_ptr, c_ptr, c_ptr, Strides, c_ptr, Strides, c_ptr, c_i64, c_i32,
                             c_i32, c_i32, c_i32, c_ptr]),
     "hata_decode_topk_attn": (c_i32, [c_ptr, c_ptr, c_ptr, Strides, c_i32, c_ptr, Strides, c_ptr, c_i32, c_i32,
@@ -48,6 +50,7 @@ _SIGS = {
     "hata_shard_partial_attn": (c_i32, [c_ptr, c_ptr, c_ptr, Strides, c_i32, c_ptr, c_ptr, c_i32, c_i32, c_i32,
                                         c_i32, c_i32, c_f32, c_ptr, c_ptr]),
     "hata_shard_combine": (c_i32, [c_ptr, c_i32, c_i32, c_i32, c_i32, c_ptr, c_i32, c_ptr]),
+    "hata_set_option": (c_i32, [c_i32, c_i32]),
     "hata_status_string": (ctypes.c_char_p, [c_i32]),
     "hata_last_error": (ctypes.c_char_p, []),
     "hata_version": (ctypes.c_char_p, []),

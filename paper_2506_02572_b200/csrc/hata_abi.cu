@@ -92,6 +92,12 @@ const char* hata_status_string(hata_status s) {
 
 const char* hata_last_error(void) { return g_last_error; }
 
+hata_status hata_set_option(hata_option opt, int value) {
+  if (opt != HATA_OPT_SELECTION_HINT && opt != HATA_OPT_PDL) return HATA_ERR_INVALID_ARG;
+  hata::set_option_value((int)opt, value ? 1 : 0);
+  return HATA_OK;
+}
+
 const char* hata_version(void) { return "libhata 0.1 (sm_100a)"; }
 
 hata_status hata_debug_trace(void* buf) { return cuda_status(hata::set_decode_trace(buf)); }
@@ -102,11 +108,12 @@ hata_status hata_debug_timestamp(void* dst, hata_stream_t stream) {
 }
 
 hata_status hata_hash_keys(const void* K, hata_strides ks, hata_dtype dt, const void* W, int B, int H_kv, int d,
-                           int rbits, int64_t t0, int64_t n, uint32_t* codes, hata_strides cs,
+                           int rbits, int64_t t0, int64_t n, int64_t cap, uint32_t* codes, hata_strides cs,
                            hata_stream_t stream) {
   if (!K || !W || !codes || B < 1 || H_kv < 1 || d < 1 || rbits < 32 || rbits % 32 || t0 < 0 || n < 0 ||
       !dtype_ok(dt))
     return HATA_ERR_INVALID_ARG;
+  if (t0 + n > cap) return HATA_ERR_CAPACITY;
   if (!shape_supported(d, rbits, 1)) return HATA_ERR_UNSUPPORTED;
   if (!kv_layout_ok(K, ks, elem_bytes(dt), d) || cs.st != rbits / 32 || !aligned(codes, 4) || !aligned(W, 16))
     return HATA_ERR_INVALID_ARG;
@@ -157,7 +164,8 @@ static hata_status decode_common(const void* q, const void* K, const void* V, ha
                                  int d, int rbits, const int64_t* n, int64_t n_max, int k, float scale, void* out,
                                  hata_dtype out_dt, int32_t* out_idx, int32_t* out_score, uint32_t* out_qcodes,
                                  void* workspace, size_t ws_bytes, int cand_mode, int64_t token_offset,
-                                 int32_t* cand_D, const void* k_new, const void* v_new, hata_stream_t stream) {
+                                 int32_t* cand_D, const void* k_new, const void* v_new, int64_t cap,
+                                 hata_stream_t stream) {
   if (!q || !codes || !W || !n || B < 1 || H_kv < 1 || H_q < H_kv || H_q % H_kv || rbits < 32 || rbits % 32 ||
       n_max < 0 || k < 1 || !dtype_ok(dt))
     return HATA_ERR_INVALID_ARG;
@@ -179,7 +187,7 @@ static hata_status decode_common(const void* q, const void* K, const void* V, ha
   p.out = out; p.out_bf16 = out_dt == HATA_BF16;
   p.out_idx = out_idx; p.out_score = out_score; p.out_qcodes = out_qcodes;
   p.cand_mode = cand_mode; p.token_offset = token_offset; p.cand_D = cand_D;
-  p.k_new = k_new; p.v_new = v_new;
+  p.k_new = k_new; p.v_new = v_new; p.cap = cap;
   return cuda_status(hata::launch_decode(p, pl, workspace, dt == HATA_BF16, reinterpret_cast<cudaStream_t>(stream)));
 }
 
@@ -189,7 +197,7 @@ hata_status hata_decode_topk_attn(const void* q, const void* K, const void* V, h
                                   hata_dtype out_dt, int32_t* out_idx, int32_t* out_score, uint32_t* out_qcodes,
                                   void* workspace, size_t ws_bytes, hata_stream_t stream) {
   return decode_common(q, K, V, kvs, dt, codes, cs, W, B, H_q, H_kv, d, rbits, n, n_max, k, scale, out, out_dt,
-                       out_idx, out_score, out_qcodes, workspace, ws_bytes, 0, 0, nullptr, nullptr, nullptr, stream);
+                       out_idx, out_score, out_qcodes, workspace, ws_bytes, 0, 0, nullptr, nullptr, nullptr, n_max, stream);
 }
 
 hata_status hata_decode_step(const void* q, const void* k_new, const void* v_new, void* K, void* V, hata_strides kvs,
@@ -201,7 +209,7 @@ hata_status hata_decode_step(const void* q, const void* k_new, const void* v_new
   if (n_max > cap) return HATA_ERR_CAPACITY;
   if (!aligned(k_new, 16) || !aligned(v_new, 16)) return HATA_ERR_INVALID_ARG;
   return decode_common(q, K, V, kvs, dt, codes, cs, W, B, H_q, H_kv, d, rbits, n, n_max, k, scale, out, out_dt,
-                       out_idx, out_score, out_qcodes, workspace, ws_bytes, 0, 0, nullptr, k_new, v_new, stream);
+                       out_idx, out_score, out_qcodes, workspace, ws_bytes, 0, 0, nullptr, k_new, v_new, cap, stream);
 }
 
 hata_status hata_shard_candidates(const void* q, hata_dtype dt, const uint32_t* codes, hata_strides cs,
@@ -213,7 +221,7 @@ hata_status hata_shard_candidates(const void* q, hata_dtype dt, const uint32_t* 
   hata_strides none = {0, 0, 0};
   return decode_common(q, nullptr, nullptr, none, dt, codes, cs, W, B, H_q, H_kv, d, rbits, n_local, n_local_max, k,
                        0.f, nullptr, HATA_F32, cand_idx, nullptr, nullptr, workspace, ws_bytes, 1, token_offset,
-                       cand_D, nullptr, nullptr, stream);
+                       cand_D, nullptr, nullptr, n_local_max, stream);
 }
 
 hata_status hata_shard_select(const int32_t* all_D, const int32_t* all_idx, int P, int B, int H_kv, int k, int G,

@@ -1,4 +1,5 @@
 // Host-side planning + dispatch of the fused decode kernel (hata_decode.cuh).
+#include <atomic>
 #include <cstdlib>
 #include "hata_internal.h"
 #include "hata_decode_kernel.cuh"
@@ -70,10 +71,13 @@ DecodePlan plan_decode(int B, int Hq, int Hkv, int d, int rbits, int64_t n_max, 
   if (M > DEC_MAX_RANKS) M = DEC_MAX_RANKS;
   const int64_t by_len = (n_max + 1023) / 1024;          // >= 1024 tokens per rank
   if (by_len < M) M = (int)(by_len < 1 ? 1 : by_len);
+#if HATA_DIAG
+  // diagnostics build only: force the rank count
   if (const char* e = std::getenv("HATA_RANKS")) {
     const int v = std::atoi(e);
     if (v >= 1 && v <= DEC_MAX_RANKS && v * units <= sms) M = v;
   }
+#endif
   const int rowb = d * eb + DEC_ROW_PAD;
   const int wbytes = (d * dec_wrow_stride(rbits, eb) + 127) & ~127;
   for (;;) {
@@ -117,11 +121,16 @@ DecodePlan plan_decode(int B, int Hq, int Hkv, int d, int rbits, int64_t n_max, 
     break;
   }
   const int hs = dec_hist_stride(pl.nbins + 1);
-  // workspace (every section 256-byte aligned)
+  // workspace (every section 256-byte aligned).  The sections that carry
+  // state from one launch to the next -- the sync words (zero between
+  // launches, plus the threshold hint) and the unit totals (zero between
+  // launches) -- come first, at offsets that depend only on (B*H_kv, G*rbits),
+  // so a workspace may be reused while n_max (hence M) and k change; the
+  // sections after them are fully written before they are read in a launch.
   size_t off = 0;
   pl.ws_sync = off;  off += up256((size_t)units * 4 * 4);          // [2] = threshold hint (any M)
+  pl.ws_tot = off;   off += up256((size_t)units * hs * 4);
   pl.ws_hist = off;  off += M > 1 ? up256((size_t)units * M * hs * 4) : 0;
-  pl.ws_tot = off;   off += M > 1 ? up256((size_t)units * hs * 4) : 0;
   pl.ws_part = off;  off += M > 1 ? up256((size_t)units * M * dec_part_stride(GT, d) * 4) : 0;
   pl.ws_D = off;     off += !pl.d_smem ? up256((size_t)units * M * dec_dchunk(pl.chunk) * 2) : 0;
   pl.ws_rows = off;  off += pl.rows_global ? up256((size_t)units * M * pl.R_cap * 4) : 0;
@@ -134,8 +143,12 @@ cudaError_t launch_decode(DecodeParams& p, const DecodePlan& pl, void* ws, int i
   if (!kern) return cudaErrorNotSupported;
   uint8_t* w = reinterpret_cast<uint8_t*>(ws);
   p.trace = decode_trace_buf();
-  { const char* e = std::getenv("HATA_DEBUG"); p.dbg = e ? std::atoi(e) : 0; }
-  { static const int h = [] { const char* e = std::getenv("HATA_HINT"); return e ? std::atoi(e) : 1; }(); p.use_hint = h; }
+#if HATA_DIAG
+  { const char* e = std::getenv("HATA_DEBUG"); p.dbg = e ? std::atoi(e) : 0; }   // diagnostics build only
+#else
+  p.dbg = 0;
+#endif
+  p.use_hint = option_value(OPT_SELECTION_HINT);
   p.M = pl.M; p.stages = pl.stages; p.chunk = pl.chunk; p.nbins = pl.nbins; p.rows_cap = pl.rows_cap; p.R_cap = pl.R_cap;
   p.d_smem = pl.d_smem;
   p.ws_sync = reinterpret_cast<unsigned*>(w + pl.ws_sync);
@@ -154,14 +167,13 @@ cudaError_t launch_decode(DecodeParams& p, const DecodePlan& pl, void* ws, int i
   cfg.stream = s;
   // ranks of a unit meet at a spin barrier: they must be co-resident
   at[0].id = cudaLaunchAttributeCooperative;
-  at[0].val.cooperative = (pl.M > 1 && !(p.dbg & 8)) ? 1 : 0;
+  at[0].val.cooperative = pl.M > 1 ? 1 : 0;
   cfg.attrs = at;
   cfg.numAttrs = 1;
   // programmatic dependent launch: the prologue (barrier init, W_g loads)
   // overlaps the tail of the preceding kernel in the stream; the kernel waits
   // (griddepcontrol.wait) before touching anything that kernel may produce
-  static const int pdl = [] { const char* e = std::getenv("HATA_PDL"); return e ? std::atoi(e) : 1; }();
-  if (pdl) {
+  if (option_value(OPT_PDL)) {
     at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     at[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.numAttrs = 2;
@@ -204,6 +216,11 @@ cudaError_t launch_partial_attn(PartialParams& p, int GT, int is_bf16, cudaStrea
 }  // namespace hata
 
 namespace hata {
+// process-wide options (hata_set_option); defaults on
+static std::atomic<int> g_opts[OPT_COUNT] = {{1}, {1}};
+int option_value(int opt) { return (opt >= 0 && opt < OPT_COUNT) ? g_opts[opt].load(std::memory_order_relaxed) : 0; }
+void set_option_value(int opt, int v) { if (opt >= 0 && opt < OPT_COUNT) g_opts[opt].store(v, std::memory_order_relaxed); }
+
 static unsigned long long* g_trace_buf = nullptr;   // host-side: copied into DecodeParams::trace
 cudaError_t set_decode_trace(void* buf) {
   g_trace_buf = reinterpret_cast<unsigned long long*>(buf);

@@ -75,7 +75,8 @@ struct DecodeParams {
   // emit (D, global index) candidates instead of attending.
   int cand_mode;
   int64_t token_offset;    // global index of local token 0
-  int64_t n_max;           // host bound on n[b]: fixes the rank chunks (chunk = ceil(n_max/M))
+  int64_t n_max;           // host bound on n[b]: fixes the rank chunks (chunk = ceil(n_max/M)); n[b] is clamped to it
+  int64_t cap;             // rows allocated per (b, KV head): the fused append writes row n-1 only if < cap
   int32_t* cand_D;         // [B, Hkv, k] or null
   // fused append (hata_decode_step): write k_new/v_new and the key code at row
   // n[b]-1 before scoring; null = caches already hold the new token

@@ -80,33 +80,6 @@ __device__ __forceinline__ int block_excl_scan2(int a, int b, int* buf, int& eb,
   return buf[warp] + ia - a;
 }
 
-// 8-bit masks of (D < thr) and (D == thr) for tokens j .. j+7 of a chunk,
-// tokens >= s1 masked out.
-__device__ __forceinline__ void d_masks(const uint16_t* Dc, bool fromg, int j, int s1, int thr, uint32_t& ltm,
-                                        uint32_t& tim) {
-  uint32_t v[4];
-  if (j + 8 <= s1) {
-    const uint4 x = fromg ? __ldcg(reinterpret_cast<const uint4*>(Dc + j)) : *reinterpret_cast<const uint4*>(Dc + j);
-    v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
-  } else {
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const uint32_t lo = (j + 2 * e < s1) ? (uint32_t)(fromg ? __ldcg(Dc + j + 2 * e) : Dc[j + 2 * e]) : 0xffffu;
-      const uint32_t hi = (j + 2 * e + 1 < s1) ? (uint32_t)(fromg ? __ldcg(Dc + j + 2 * e + 1) : Dc[j + 2 * e + 1])
-                                               : 0xffffu;
-      v[e] = lo | (hi << 16);
-    }
-  }
-  ltm = 0;
-  tim = 0;
-#pragma unroll
-  for (int e = 0; e < 8; ++e) {
-    const int dv = (int)((v[e >> 1] >> (16 * (e & 1))) & 0xffffu);
-    ltm |= (uint32_t)(dv < thr) << e;
-    tim |= (uint32_t)(dv == thr) << e;
-  }
-}
-
 template <typename T, int W, int GT, int D_HEAD>
 __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __grid_constant__ DecodeParams p) {
   constexpr int J = sw_planes_for_group(GT);                       // signed-weight planes
@@ -193,7 +166,9 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
   // cache (a preceding decode may append to it), the workspace and every
   // global write come after the wait.  A no-op without the launch attribute.
   griddep_wait();
-  const int64_t n = p.n[b];
+  // n[b] > n_max is clamped to n_max: the rank chunks are fixed by n_max
+  // (include/hata.h documents this)
+  const int64_t n = min(p.n[b], p.n_max);
   if (tid == 0) {
     // q and the new key/value first (they gate the q-hash), then the code
     // chunk in a few large copies: a CTA's TMA requests are served in order
@@ -230,7 +205,7 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
   // also appends the new token (k_new != null), its key -- one projection pass
   // with the key as row G.  The rank owning row pos = n-1 writes K/V/code rows.
   const int64_t pos = n - 1;
-  const bool owner = append && n >= 1 && pos >= t0 && pos < t0 + Lr;
+  const bool owner = append && n >= 1 && pos < p.cap && pos >= t0 && pos < t0 + Lr;
   const int NV = G + (owner ? 1 : 0);                                // projected vectors
   mbar_wait(&bars[NST], 0);                                         // W_g in smem
   mbar_wait(&bars[NST + 1], 0);                                     // q, k_new, v_new (+ hint) in smem
@@ -470,9 +445,11 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
       asm volatile("fence.proxy.async.global;" ::: "memory");        // this rank's own gather reads it by TMA
     }
   }
-  // pad D past the valid tokens with 0x7fff (never selected) up to the
-  // selection's per-thread blocking (dec_dchunk)
-  for (int i = Lr + tid; i < dec_dchunk(Lr); i += DEC_THREADS) Dloc[i] = 0x7fffu;
+  // pad D past the valid tokens with 0x7fff (never selected) up to what the
+  // selection reads: the per-thread blocking (dec_dchunk(Lr)) of the full
+  // scan, or every bitmap word (nbw * 32 = dec_dchunk(chunk)) of the hinted path
+  const int dpad = hinted ? nbw * 32 : dec_dchunk(Lr);
+  for (int i = Lr + tid; i < dpad; i += DEC_THREADS) Dloc[i] = 0x7fffu;
   __syncthreads();
 
   // ---- phase 3: exact top-k' (Alg. 3 lines 12-13) by counting select.
@@ -500,6 +477,9 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
       mysum += tb[q];
     }
     int total;
+    // threshold slots, initialised before the scan's barriers (the M == 1
+    // threshold loop below writes them without a further barrier)
+    if (tid == 0) { misc[0] = -1; misc[1] = 0; misc[4] = p.nbins; }
     cum = block_excl_scan(mysum, misc + 16, total);                  // #{local D < i0}
   }
   auto build_bitmap = [&]() {
@@ -522,7 +502,6 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
       Bc[w] = m;
     }
   };
-  if (tid == 0) { misc[0] = -1; misc[1] = 0; misc[4] = p.nbins; }
   if (M > 1) {
     int32_t* gc = p.ws_hist + ((int64_t)u * M + r) * hs;
     int32_t* gt = p.ws_tot + (int64_t)u * hs;

@@ -41,6 +41,10 @@ struct DecodePlan {
   size_t ws_sync, ws_hist, ws_tot, ws_part, ws_D, ws_rows, ws_total;   // workspace byte offsets / size
 };
 struct DecodeParams;
+// process-wide options (hata_set_option), indices = hata_option values
+enum { OPT_SELECTION_HINT = 0, OPT_PDL = 1, OPT_COUNT = 2 };
+int option_value(int opt);
+void set_option_value(int opt, int v);
 DecodePlan plan_decode(int B, int Hq, int Hkv, int d, int rbits, int64_t n_max, int k, int elem_bytes);
 int group_template(int G);
 cudaError_t launch_decode(DecodeParams& p, const DecodePlan& plan, void* ws, int is_bf16, cudaStream_t s);

@@ -4,20 +4,16 @@
 // PAPER: Alg. 3 lines 10-11 "S <- bitcount(bitwise_xor(Q_H, K_H^cache))"
 // and P:255 "aggregate the scores S for shared KVCache" (sum over the group).
 //
-// B200 formulation: for bit b let c_b = #{h : q_h[b] = 1}.
-// Then  D(k) = sum_h popc(q_h ^ k) = sum_b (k_b ? G - c_b : c_b).
-// Store J = ceil(log2(G+1)) bit planes A_j = bit j of c, B_j = bit j of (G - c);
-// per word m_j = k ? B_j : A_j (one LOP3) and D = sum_j 2^j popc(m_j).  A
-// carry-save (full-adder LOP3) tree compresses the J*W weighted words before
-// counting, so the POPC count is ~log2(G*rbits) instead of G*W.
+// B200 formulation: for bit b let c_b = #{h : q_h[b] = 1}
+// and w_b = G - 2 c_b.  Then  D(k) = sum_h popc(q_h ^ k) = C0 + sum_b k_b w_b
+// with C0 = sum_b c_b; the weights are split into signed magnitude bit planes
+// (one LOP3 per plane and word) and a carry-save (full-adder LOP3) tree
+// compresses the weighted words before counting, so the POPC count is
+// ~log2(G*rbits) instead of G*W (group_distance_sw below).
 #pragma once
 #include "hata_common.cuh"
 
 namespace hata {
-
-constexpr __host__ __device__ int planes_for_group(int G) {
-  return G <= 1 ? 1 : (G <= 3 ? 2 : (G <= 7 ? 3 : 4));
-}
 
 // popcount of W words (weight 1) via a carry-save tree.
 template <int W>
@@ -44,44 +40,6 @@ __device__ __forceinline__ uint32_t popc_words(const uint32_t* m) {
     uint32_t twos = t ^ cd, f2 = t & cd;
     uint32_t fours = f1 ^ f2, eights = f1 & f2;
     return __popc(ones) + 2u * __popc(twos) + 4u * __popc(fours) + 8u * __popc(eights);
-  }
-}
-
-// D for one key code k[W] given planes A[J][W], B[J][W].
-template <int W, int J>
-__device__ __forceinline__ uint32_t group_distance(const uint32_t (&k)[W], const uint32_t (&A)[J][W],
-                                                   const uint32_t (&B)[J][W]) {
-  if constexpr (W == 4 && J == 3) {
-    // Cross-plane carry-save tree: 12 weighted words -> 5 counted words.
-    uint32_t m[3][4];
-#pragma unroll
-    for (int j = 0; j < 3; ++j)
-#pragma unroll
-      for (int w = 0; w < 4; ++w) m[j][w] = lop_mux(k[w], B[j][w], A[j][w]);
-    uint32_t s0, c0;
-    full_add(m[0][0], m[0][1], m[0][2], s0, c0);
-    uint32_t l0 = s0 ^ m[0][3], c0b = s0 & m[0][3];           // weight 1 | carries weight 2
-    uint32_t s1, c1, s1b, c1b;
-    full_add(m[1][0], m[1][1], m[1][2], s1, c1);
-    full_add(m[1][3], c0, c0b, s1b, c1b);
-    uint32_t l1 = s1 ^ s1b, c1c = s1 & s1b;                    // weight 2 | carries weight 4
-    uint32_t s2, c2, s2b, c2b, l2, c2c;
-    full_add(m[2][0], m[2][1], m[2][2], s2, c2);
-    full_add(m[2][3], c1, c1b, s2b, c2b);
-    full_add(s2, s2b, c1c, l2, c2c);                           // weight 4 | carries weight 8
-    uint32_t l3, l4;
-    full_add(c2, c2b, c2c, l3, l4);                            // weight 8 | weight 16
-    return __popc(l0) + 2u * __popc(l1) + 4u * __popc(l2) + 8u * __popc(l3) + 16u * __popc(l4);
-  } else {
-    uint32_t d = 0;
-#pragma unroll
-    for (int j = 0; j < J; ++j) {
-      uint32_t m[W];
-#pragma unroll
-      for (int w = 0; w < W; ++w) m[w] = lop_mux(k[w], B[j][w], A[j][w]);
-      d += popc_words<W>(m) << j;
-    }
-    return d;
   }
 }
 

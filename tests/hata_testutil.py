@@ -117,3 +117,81 @@ def check_decode(case: dict, g: dict, k: int, code_rows_sample: int | None = Non
     tol = TOL[sh.dtype]
     assert err <= tol, f"max abs err {err} > {tol}"
     return dict(code_bit_mismatch=mism, near_zero_bits=nzc, bits=bits, max_abs_err=err)
+
+
+# ------------------------------------------------------------------------
+# Large cases: inputs stay on the GPU; the oracle checks sampled (b, KV head)
+# units one by one (north_star: "at full sizes ... sampled outputs the oracle
+# can compute one by one").
+def check_units(case: dict, res: dict, k: int, units, code_rows_sample: int | None = 65536, rng_seed: int = 0,
+                n_dev=None):
+    """Parity protocol on the (b, g) units listed.  ``case`` holds the
+    generator inputs (any device); ``res`` the GPU results after the step:
+    K, V, codes (caches), out, idx, score, qc (device tensors) and n [B]."""
+    sh = case["shape"]
+    G, Wd = sh.G, sh.rbits // 32
+    n = res["n"].cpu().numpy()
+    rng = np.random.default_rng(rng_seed)
+    errs = []
+    for (b, g) in units:
+        nb = int(n[b])
+        W64 = to_np64(case["W"][g])
+        # oracle caches of this unit: generator rows + Alg. 3 line 3-4 append at nb-1
+        K64 = to_np64(case["K"][b, g, :nb]); V64 = to_np64(case["V"][b, g, :nb])
+        if nb >= 1:
+            K64[nb - 1] = to_np64(case["k_new"][b, g]); V64[nb - 1] = to_np64(case["v_new"][b, g])
+        assert np.array_equal(to_np64(res["K"][b, g, :nb]), K64), f"K cache differs at {(b, g)}"
+        assert np.array_equal(to_np64(res["V"][b, g, :nb]), V64), f"V cache differs at {(b, g)}"
+        codes = codes_u32(res["codes"][b, g, :nb])
+        rows = None
+        if code_rows_sample and nb > code_rows_sample:
+            rows = np.sort(rng.choice(nb, size=code_rows_sample, replace=False))
+            rows[-1] = nb - 1
+        if nb:
+            check_codes(codes, K64, W64, rows)
+        q64 = to_np64(case["q"][b, g * G:(g + 1) * G])
+        qg = codes_u32(res["qc"][b, g * G:(g + 1) * G])
+        qref, qnz = O.hash_encode(q64, W64)
+        qdiff = O.bit_unpack(qref, sh.rbits) != O.bit_unpack(qg, sh.rbits)
+        assert not np.any(qdiff & ~qnz), f"query code bits differ outside the near-zero band at {(b, g)}"
+        # protocol step 2 on this unit as a one-unit problem (B = 1, H_kv = 1)
+        r1 = O.decode(q64[None], K64[None, None], V64[None, None], codes[None, None], W64[None], np.array([nb]), k,
+                      qc=qg[None])
+        kp = min(k, nb)
+        idx = res["idx"][b, g].cpu().numpy()
+        sc = res["score"][b, g].cpu().numpy()
+        assert np.array_equal(idx[:kp], r1["idx"][0][0]), f"index set differs at {(b, g)}"
+        assert np.all(idx[kp:] == -1)
+        assert np.array_equal(sc[:kp], r1["S"][0][0]), f"scores differ at {(b, g)}"
+        out = res["out"][b, g * G:(g + 1) * G].double().cpu().numpy()
+        ref = r1["out"][0] if nb else np.zeros_like(out)
+        err = float(np.max(np.abs(out - ref)))
+        assert err <= TOL[sh.dtype], f"max abs err {err} at {(b, g)}"
+        errs.append(err)
+    return dict(units=len(units), max_abs_err=max(errs) if errs else 0.0)
+
+
+def resident_setup(case: dict, n_before, kv_pair=False, device="cuda"):
+    """Device caches for ``case`` (already on ``device``) with rows [0, n_before)
+    hashed by hata_hash_keys; returns dict(K, V, codes, W, nb)."""
+    import paper_2506_02572_b200 as H
+    sh = case["shape"]
+    K, V = case["K"].to(device), case["V"].to(device)
+    if kv_pair:
+        kv = torch.stack((K, V), dim=3)
+        K, V = kv[:, :, :, 0, :], kv[:, :, :, 1, :]
+    else:
+        K, V = K.clone(), V.clone()
+    W = case["W"].to(device).contiguous()
+    B, Hkv, cap, d = K.shape
+    codes = torch.zeros(B, Hkv, cap, sh.rbits // 32, dtype=torch.int32, device=device)
+    nb = n_before.to(device)
+    H.hash_keys(K, W, codes, 0, int(nb.max().item()))
+    return dict(K=K, V=V, codes=codes, W=W, nb=nb)
+
+
+def new_outputs(sh, k, device="cuda", out_dtype=torch.float32):
+    return dict(out=torch.empty(sh.B, sh.Hq, sh.d, dtype=out_dtype, device=device),
+                idx=torch.full((sh.B, sh.Hkv, k), -7, dtype=torch.int32, device=device),
+                score=torch.zeros(sh.B, sh.Hkv, k, dtype=torch.int32, device=device),
+                qc=torch.zeros(sh.B, sh.Hq, sh.rbits // 32, dtype=torch.int32, device=device))

@@ -55,9 +55,14 @@ def test_validation_rejects_before_launch(lib):
     assert lib.hata_decode_topk_attn(P, P, P, s, 1, P, s, P, 1, 30, 8, 128, 128, P, 100, 4, 0.0, P, 0,
                                      None, None, None, None, 0, None) == 1
     # rbits % 32 != 0
-    assert lib.hata_hash_keys(P, Strides(1, 1, 128), 1, P, 1, 1, 128, 100, 0, 10, P, Strides(1, 1, 4), None) == 1
+    assert lib.hata_hash_keys(P, Strides(1, 1, 128), 1, P, 1, 1, 128, 100, 0, 10, 16, P, Strides(1, 1, 4), None) == 1
     # unsupported head dim
-    assert lib.hata_hash_keys(P, Strides(1, 1, 64), 1, P, 1, 1, 64, 128, 0, 10, P, Strides(1, 1, 4), None) == 2
+    assert lib.hata_hash_keys(P, Strides(1, 1, 64), 1, P, 1, 1, 64, 128, 0, 10, 16, P, Strides(1, 1, 4), None) == 2
+    # t0 + n beyond the capacity
+    assert lib.hata_hash_keys(P, Strides(1, 1, 128), 1, P, 1, 1, 128, 128, 8, 10, 16, P, Strides(1, 1, 4), None) == 3
+    # unknown option; known options accepted
+    assert lib.hata_set_option(7, 1) == 1
+    assert lib.hata_set_option(0, 1) == 0 and lib.hata_set_option(1, 1) == 0
     # null pointers
     assert lib.hata_append(None, P, 1, P, P, P, s, P, s, P, 10, 1, 1, 128, 128, None) == 1
     assert lib.hata_shard_combine(None, 2, 1, 32, 128, P, 0, None) == 1
@@ -76,3 +81,12 @@ def test_workspace_query(lib):
     assert decode_ranks(16, 32, 8, 128, 128, 131072, 2048) == 1
     assert decode_workspace_size(16, 32, 8, 128, 128, 131072, 2048) >= 128 * 131072 * 2
     assert decode_workspace_size(1, 32, 8, 128, 100, 1000, 10) == 0  # invalid -> 0
+
+
+def test_product_library_reads_no_debug_env(lib):
+    """The diagnostics knobs (rank count, debug bits) live only in the
+    diagnostics build; the product library reads no HATA_* environment."""
+    from paper_2506_02572_b200 import _lib
+    data = open(_lib.LIB_PATH, "rb").read()
+    for knob in (b"HATA_RANKS", b"HATA_DEBUG", b"HATA_HINT", b"HATA_PDL"):
+        assert knob not in data, knob
