@@ -45,6 +45,10 @@ def _strides4(t: torch.Tensor) -> Strides:
 
 
 def _p(t):
+    """Device pointer of ``t``.  Callers pass tensors that stay referenced
+    until the call returns: a temporary (e.g. ``x.contiguous()``) freed before
+    the asynchronous launch may be handed by the caching allocator to the next
+    copy on the stream and overwritten before the kernel reads it."""
     return None if t is None else t.data_ptr()
 
 
@@ -69,10 +73,11 @@ def set_option(name: str, value: int):
 def hash_keys(K, W, codes, t0: int = 0, n: int | None = None, stream=None):
     """Alg. 1 lines 2-5: codes[:, :, t0:t0+n] = HashEncode(K[:, :, t0:t0+n]) (in place)."""
     _need_cuda(K, W, codes)
+    W = W.contiguous()
     B, Hkv, cap, d = K.shape
     rbits = W.shape[2]
     n = cap - t0 if n is None else n
-    _lib.check(lib().hata_hash_keys(_p(K), _strides4(K), _dt(K), _p(W.contiguous()), B, Hkv, d, rbits, t0, n, cap,
+    _lib.check(lib().hata_hash_keys(_p(K), _strides4(K), _dt(K), _p(W), B, Hkv, d, rbits, t0, n, cap,
                                     _p(codes), _strides4(codes), _stream(stream)), "hata_hash_keys")
     return codes
 
@@ -80,10 +85,11 @@ def hash_keys(K, W, codes, t0: int = 0, n: int | None = None, stream=None):
 def append(k_new, v_new, W, K, V, codes, pos, stream=None):
     """Alg. 3 lines 2-9: write k_new/v_new and HashEncode(k_new) at row pos[b] (in place)."""
     _need_cuda(k_new, v_new, W, K, V, codes, pos)
+    k_new, v_new = k_new.contiguous(), v_new.contiguous()
     B, Hkv, cap, d = K.shape
     if K.stride() != V.stride():
         raise HataError("K and V must share strides")
-    _lib.check(lib().hata_append(_p(k_new.contiguous()), _p(v_new.contiguous()), _dt(K), _p(W), _p(K), _p(V),
+    _lib.check(lib().hata_append(_p(k_new), _p(v_new), _dt(K), _p(W), _p(K), _p(V),
                                  _strides4(K), _p(codes), _strides4(codes), _p(pos), cap, B, Hkv, d, W.shape[2],
                                  _stream(stream)), "hata_append")
 
@@ -102,6 +108,7 @@ def decode_topk_attn(q, K, V, codes, W, n, k: int, n_max: int | None = None, sca
     """Alg. 3 lines 6, 10-17 over caches already holding the new token.
     Returns ``out`` [B, H_q, d]."""
     _need_cuda(q, K, V, codes, W, n)
+    q = q.contiguous()
     B, Hq, d = q.shape
     Hkv, rbits = K.shape[1], W.shape[2]
     if n_max is None:
@@ -114,7 +121,7 @@ def decode_topk_attn(q, K, V, codes, W, n, k: int, n_max: int | None = None, sca
     if ws and (workspace is None or workspace.numel() * workspace.element_size() < ws):
         workspace = torch.zeros(ws, dtype=torch.uint8, device=q.device)
     _lib.check(lib().hata_decode_topk_attn(
-        _p(q.contiguous()), _p(K), _p(V), _strides4(K), _dt(K), _p(codes), _strides4(codes), _p(W), B, Hq, Hkv, d,
+        _p(q), _p(K), _p(V), _strides4(K), _dt(K), _p(codes), _strides4(codes), _p(W), B, Hq, Hkv, d,
         rbits, _p(n), n_max, k, scale, _p(out), _dt(out), _p(out_idx), _p(out_score), _p(out_qcodes),
         _p(workspace) if ws else None, ws, _stream(stream)), "hata_decode_topk_attn")
     return out
@@ -126,6 +133,7 @@ def decode_step(q, k_new, v_new, K, V, codes, W, n, k: int, n_max: int | None = 
     """Alg. 3 lines 2-17 in one launch: append k_new/v_new (and the key code) at
     row n[b]-1, then decode.  ``n`` counts the new token.  Returns ``out``."""
     _need_cuda(q, k_new, v_new, K, V, codes, W, n)
+    q, k_new, v_new = q.contiguous(), k_new.contiguous(), v_new.contiguous()
     B, Hq, d = q.shape
     Hkv, cap, rbits = K.shape[1], K.shape[2], W.shape[2]
     if n_max is None:
@@ -138,7 +146,7 @@ def decode_step(q, k_new, v_new, K, V, codes, W, n, k: int, n_max: int | None = 
     if ws and (workspace is None or workspace.numel() * workspace.element_size() < ws):
         workspace = torch.zeros(ws, dtype=torch.uint8, device=q.device)
     _lib.check(lib().hata_decode_step(
-        _p(q.contiguous()), _p(k_new.contiguous()), _p(v_new.contiguous()), _p(K), _p(V), _strides4(K), _dt(K),
+        _p(q), _p(k_new), _p(v_new), _p(K), _p(V), _strides4(K), _dt(K),
         _p(codes), _strides4(codes), _p(W), B, Hq, Hkv, d, rbits, _p(n), n_max, cap, k, scale, _p(out), _dt(out),
         _p(out_idx), _p(out_score), _p(out_qcodes), _p(workspace) if ws else None, ws, _stream(stream)),
         "hata_decode_step")
@@ -148,13 +156,14 @@ def decode_step(q, k_new, v_new, K, V, codes, W, n, k: int, n_max: int | None = 
 def shard_candidates(q, codes, W, n_local, n_local_max: int, token_offset: int, k: int, cand_D, cand_idx,
                      workspace=None, stream=None):
     _need_cuda(q, codes, W, n_local, cand_D, cand_idx)
+    q = q.contiguous()
     B, Hq, d = q.shape
     Hkv, rbits = codes.shape[1], W.shape[2]
     ws = decode_workspace_size(B, Hq, Hkv, d, rbits, n_local_max, k, q.dtype)
     if ws and (workspace is None or workspace.numel() * workspace.element_size() < ws):
         workspace = torch.zeros(ws, dtype=torch.uint8, device=q.device)
     _lib.check(lib().hata_shard_candidates(
-        _p(q.contiguous()), _dt(q), _p(codes), _strides4(codes), _p(W), B, Hq, Hkv, d, rbits, _p(n_local),
+        _p(q), _dt(q), _p(codes), _strides4(codes), _p(W), B, Hq, Hkv, d, rbits, _p(n_local),
         n_local_max, token_offset, k, _p(cand_D), _p(cand_idx), _p(workspace) if ws else None, ws,
         _stream(stream)), "hata_shard_candidates")
 
@@ -170,9 +179,10 @@ def shard_select(all_D, all_idx, n_total, lo: int, hi: int, G: int, rbits: int, 
 
 def shard_partial_attn(q, K, V, own_idx, own_cnt, k: int, partial, scale: float = 0.0, stream=None):
     _need_cuda(q, K, V, own_idx, own_cnt, partial)
+    q = q.contiguous()
     B, Hq, d = q.shape
     Hkv = K.shape[1]
-    _lib.check(lib().hata_shard_partial_attn(_p(q.contiguous()), _p(K), _p(V), _strides4(K), _dt(K), _p(own_idx),
+    _lib.check(lib().hata_shard_partial_attn(_p(q), _p(K), _p(V), _strides4(K), _dt(K), _p(own_idx),
                                              _p(own_cnt), B, Hq, Hkv, d, k, scale, _p(partial), _stream(stream)),
                "hata_shard_partial_attn")
 

@@ -184,3 +184,27 @@ def test_workspace_reused_while_n_max_changes():
         ref["v_new"] = case["V"][:, :, n_max - 1].clone() if n_max < sh.N else case["v_new"]
         print(n_max, check_units(ref, _res(st, o, n), sh.k, [(0, 0), (0, 4), (0, 7)]))
     assert len(Ms) >= 3
+
+
+def test_noncontiguous_inputs_equal_contiguous():
+    """Non-contiguous q / k_new / v_new (head slices of larger tensors) are
+    copied by the binding; the copies must stay alive until the launch has
+    read them (a freed temporary was once reused by the next copy, so the
+    appended K row held v_new)."""
+    sh = _shape("cfg2", B=2, N=4096, k=128)
+    big = synth.make_case(_shape("cfg2", B=2, Hq=64, Hkv=16, N=4096, k=128), seed=37, device="cuda")
+    case = dict(big, q=big["q"][:, 32:], k_new=big["k_new"][:, 8:], v_new=big["v_new"][:, 8:],
+                K=big["K"][:, 8:].contiguous(), V=big["V"][:, 8:].contiguous(), W=big["W"][8:].contiguous(), shape=sh)
+    assert not case["q"].is_contiguous() and not case["k_new"].is_contiguous()
+    outs = []
+    for contig in (False, True):
+        c = dict(case)
+        if contig:
+            c.update(q=case["q"].contiguous(), k_new=case["k_new"].contiguous(), v_new=case["v_new"].contiguous())
+        st = resident_setup(c, c["n_before"])
+        o = new_outputs(sh, sh.k)
+        _fused(c, st, o, st["nb"] + 1, sh.k, sh.N, None)
+        torch.cuda.synchronize()
+        assert torch.equal(st["K"][:, :, sh.N - 1], case["k_new"]) and torch.equal(st["V"][:, :, sh.N - 1], case["v_new"])
+        outs.append((o["out"].clone(), o["idx"].clone()))
+    assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])
