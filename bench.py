@@ -191,6 +191,19 @@ def _soak(graphs, seconds):
         torch.cuda.synchronize()
 
 
+def apply_options():
+    """Bench-side A/B switches (the library itself reads no environment):
+    HATA_BENCH_HINT / HATA_BENCH_PDL = 0 turn the option off, HATA_BENCH_COOP = 1 on."""
+    import paper_2506_02572_b200 as H
+    opts = {}
+    for name, env in (("selection_hint", "HATA_BENCH_HINT"), ("pdl", "HATA_BENCH_PDL"),
+                      ("cooperative", "HATA_BENCH_COOP")):
+        v = int(os.environ.get(env, "0" if name == "cooperative" else "1"))
+        H.set_option(name, v)
+        opts[name] = bool(v)
+    return opts
+
+
 def bench_single(sh, steps, warmup, device, n_sets=N_SETS):
     """One CUDA graph holds n_sets consecutive decode steps over n_sets distinct
     caches -- the way a model's decode step captures its attention layers in
@@ -507,6 +520,7 @@ def main():
         return
     device = torch.device("cuda", 0)
     torch.cuda.set_device(device)
+    opts = apply_options()
     peak, peak_src = _peaks()
     r = bench_single(sh, args.steps, args.warmup, device)
     steps = r["steps"]                                 # args.steps rounded up to whole graphs
@@ -527,10 +541,10 @@ def main():
                          f"> 126 MB L2)", "parallelism": "single GPU",
                    "graph": f"{N_SETS} consecutive steps (one per cache set, like the attention layers of one "
                             f"model decode step) per CUDA graph",
-                   "pdl": os.environ.get("HATA_PDL", "1") != "0",
+                   "pdl": opts["pdl"], "cooperative": opts["cooperative"],
                    "pdl_note": "programmatic dependent launch: a step's barrier init + W_g loads overlap the previous "
                                "step's tail; q, k_new, v_new, codes, workspace are read only after griddepcontrol.wait",
-                   "selection_hint": os.environ.get("HATA_HINT", "1") != "0",
+                   "selection_hint": opts["selection_hint"],
                    "kv_layout": "[B, H_kv, cap, 2, d] (K and V rows of a token adjacent)" if KV_LAYOUT == "pair"
                    else "separate K and V [B, H_kv, cap, d]"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,

@@ -135,10 +135,17 @@ hata_status hata_append(const void* k_new, const void* v_new, hata_dtype dt, con
  *              work, never the result; keep one workspace per attention
  *              layer to keep the hint per layer.  May be NULL when the size
  *              is 0.
- * Launched with programmatic dependent launch: the kernel reads W before
- * griddepcontrol.wait and everything else (q, k_new, v_new, n, codes, K/V,
- * workspace) after it.
- * One cooperative kernel launch of M x (B*H_kv) CTAs (hata_decode_ranks()).
+ * Launched with programmatic dependent launch (hata_set_option): the kernel
+ * streams W and the code rows [0, n_max) into shared memory BEFORE
+ * griddepcontrol.wait (they do not depend on q) and reads everything else
+ * (q, k_new, v_new, n, K/V, workspace) after it.  Contract: a kernel that
+ * precedes this launch in the stream and writes code rows must make those
+ * writes visible (__threadfence) before it triggers programmatic completion;
+ * every libhata kernel does (fence, then griddepcontrol.launch_dependents),
+ * and a kernel that never triggers is complete before this one starts.  The
+ * row a fused decode step appends itself is rescored from its own k_new.
+ * One kernel launch of M x (B*H_kv) CTAs (hata_decode_ranks()), at most one
+ * per SM; cooperative when HATA_OPT_COOPERATIVE is set.
  * Errors: INVALID_ARG (k < 1, H_q % H_kv, rbits % 32, n_max < 0, nulls),
  *         UNSUPPORTED, WORKSPACE, CUDA.  n[b] == 0 yields zero output and
  *         out_idx all -1.
@@ -223,7 +230,8 @@ hata_status hata_shard_combine(const float* partials, int P, int B, int H_q, int
                                hata_stream_t stream);
 
 /* ------------------------------------------------------------------------
- * Process-wide options of the decode launches (default: all on).
+ * Process-wide options of the decode launches (defaults: hint 1, PDL 1,
+ * cooperative 0).
  *   HATA_OPT_SELECTION_HINT  1: use the previous launch's threshold kept in the
  *                            workspace to visit only candidate tokens in the
  *                            select (changes the work, never the result);
@@ -231,10 +239,20 @@ hata_status hata_shard_combine(const float* partials, int P, int B, int H_q, int
  *   HATA_OPT_PDL             1: launch with programmatic dependent launch (the
  *                            prologue overlaps the preceding kernel); 0: plain
  *                            stream order.
+ *   HATA_OPT_COOPERATIVE     1: decode grids whose ranks exchange (M > 1) are
+ *                            cooperative launches (co-residency guaranteed by
+ *                            the runtime; a cooperative grid starts only when
+ *                            every SM it needs is free, so its prologue cannot
+ *                            overlap the preceding kernel); 0: plain launches
+ *                            -- the plan never exceeds one CTA per SM, so the
+ *                            grid becomes co-resident once the SMs are free,
+ *                            but a kernel that holds SMs indefinitely on a
+ *                            concurrent stream could stall the ranks' barrier
+ *                            (a bounded spin then traps).
  * Returns INVALID_ARG for an unknown option.  Thread safe; affects launches
  * enqueued after the call.
  * ------------------------------------------------------------------------ */
-typedef enum { HATA_OPT_SELECTION_HINT = 0, HATA_OPT_PDL = 1 } hata_option;
+typedef enum { HATA_OPT_SELECTION_HINT = 0, HATA_OPT_PDL = 1, HATA_OPT_COOPERATIVE = 2 } hata_option;
 hata_status hata_set_option(hata_option opt, int value);
 
 /* ------------------------------------------------------------------------ */

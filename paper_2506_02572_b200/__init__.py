@@ -65,8 +65,9 @@ def _need_cuda(*ts):
 
 
 def set_option(name: str, value: int):
-    """hata_set_option: "selection_hint" or "pdl" (process-wide, default on)."""
-    opt = {"selection_hint": _lib.HATA_OPT_SELECTION_HINT, "pdl": _lib.HATA_OPT_PDL}[name]
+    """hata_set_option: "selection_hint", "pdl" or "cooperative" (process-wide, default on)."""
+    opt = {"selection_hint": _lib.HATA_OPT_SELECTION_HINT, "pdl": _lib.HATA_OPT_PDL,
+           "cooperative": _lib.HATA_OPT_COOPERATIVE}[name]
     _lib.check(lib().hata_set_option(opt, int(value)), "hata_set_option")
 
 

@@ -18,6 +18,7 @@ HATA_F32 = 0
 HATA_BF16 = 1
 HATA_OPT_SELECTION_HINT = 0
 HATA_OPT_PDL = 1
+HATA_OPT_COOPERATIVE = 2
 
 c_i32 = ctypes.c_int
 c_i64 = ctypes.c_int64

@@ -93,7 +93,7 @@ const char* hata_status_string(hata_status s) {
 const char* hata_last_error(void) { return g_last_error; }
 
 hata_status hata_set_option(hata_option opt, int value) {
-  if (opt != HATA_OPT_SELECTION_HINT && opt != HATA_OPT_PDL) return HATA_ERR_INVALID_ARG;
+  if (opt != HATA_OPT_SELECTION_HINT && opt != HATA_OPT_PDL && opt != HATA_OPT_COOPERATIVE) return HATA_ERR_INVALID_ARG;
   hata::set_option_value((int)opt, value ? 1 : 0);
   return HATA_OK;
 }

@@ -29,6 +29,7 @@ int group_template(int G) {
 
 typedef void (*DecodeKernel)(const DecodeParams);
 
+#if !HATA_ONLY_HOT
 template <typename T, int W>
 static DecodeKernel pick_gt(int GT) {
   switch (GT) {
@@ -50,8 +51,15 @@ static DecodeKernel pick_w(int W, int GT) {
   }
   return nullptr;
 }
+#endif
 static DecodeKernel get_kernel(int is_bf16, int W, int GT) {
+#if HATA_ONLY_HOT
+  // experimental builds (HATA_DEFS=-DHATA_ONLY_HOT=1): only the bf16,
+  // rbits = 128, G = 4 instantiation (the CFG-2/3/4 shape), for fast A/B builds
+  return (is_bf16 && W == 4 && GT == 4) ? hata_decode_kernel<__nv_bfloat16, 4, 4, 128> : nullptr;
+#else
   return is_bf16 ? pick_w<__nv_bfloat16>(W, GT) : pick_w<float>(W, GT);
+#endif
 }
 
 static size_t up256(size_t x) { return (x + 255) / 256 * 256; }
@@ -121,15 +129,14 @@ DecodePlan plan_decode(int B, int Hq, int Hkv, int d, int rbits, int64_t n_max, 
     break;
   }
   const int hs = dec_hist_stride(pl.nbins + 1);
-  // workspace (every section 256-byte aligned).  The sections that carry
-  // state from one launch to the next -- the sync words (zero between
-  // launches, plus the threshold hint) and the unit totals (zero between
-  // launches) -- come first, at offsets that depend only on (B*H_kv, G*rbits),
-  // so a workspace may be reused while n_max (hence M) and k change; the
-  // sections after them are fully written before they are read in a launch.
+  // workspace (every section 256-byte aligned).  The one section that
+  // carries state from one launch to the next -- the sync words (zero
+  // between launches, plus the threshold hint) -- comes first, at an offset
+  // that does not depend on the shape, so a workspace may be reused while
+  // n_max (hence M) and k change; the sections after it are fully written
+  // before they are read in a launch.
   size_t off = 0;
   pl.ws_sync = off;  off += up256((size_t)units * 4 * 4);          // [2] = threshold hint (any M)
-  pl.ws_tot = off;   off += up256((size_t)units * hs * 4);
   pl.ws_hist = off;  off += M > 1 ? up256((size_t)units * M * hs * 4) : 0;
   pl.ws_part = off;  off += M > 1 ? up256((size_t)units * M * dec_part_stride(GT, d) * 4) : 0;
   pl.ws_D = off;     off += !pl.d_smem ? up256((size_t)units * M * dec_dchunk(pl.chunk) * 2) : 0;
@@ -154,7 +161,6 @@ cudaError_t launch_decode(DecodeParams& p, const DecodePlan& pl, void* ws, int i
   p.ws_sync = reinterpret_cast<unsigned*>(w + pl.ws_sync);
   p.ws_hist = pl.M > 1 ? reinterpret_cast<int32_t*>(w + pl.ws_hist) : nullptr;
   p.ws_part = pl.M > 1 ? reinterpret_cast<float*>(w + pl.ws_part) : nullptr;
-  p.ws_tot = pl.M > 1 ? reinterpret_cast<int32_t*>(w + pl.ws_tot) : nullptr;
   p.ws_D = !pl.d_smem ? reinterpret_cast<uint16_t*>(w + pl.ws_D) : nullptr;
   p.ws_rows = pl.rows_global ? reinterpret_cast<int32_t*>(w + pl.ws_rows) : nullptr;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, pl.smem);
@@ -165,9 +171,14 @@ cudaError_t launch_decode(DecodeParams& p, const DecodePlan& pl, void* ws, int i
   cfg.blockDim = dim3(DEC_THREADS);
   cfg.dynamicSmemBytes = pl.smem;
   cfg.stream = s;
-  // ranks of a unit meet at a spin barrier: they must be co-resident
+  // ranks of a unit meet at a spin barrier: they must be co-resident.  The
+  // plan keeps the grid within one CTA per SM, so a plain launch is
+  // co-resident as soon as the SMs are free; a cooperative launch guarantees
+  // it, but then cannot start any CTA before every SM is free -- which rules
+  // out overlapping the prologue (W_g, the code stream) with the preceding
+  // kernel's tail under programmatic dependent launch (HATA_OPT_COOPERATIVE)
   at[0].id = cudaLaunchAttributeCooperative;
-  at[0].val.cooperative = pl.M > 1 ? 1 : 0;
+  at[0].val.cooperative = (pl.M > 1 && option_value(OPT_COOPERATIVE)) ? 1 : 0;
   cfg.attrs = at;
   cfg.numAttrs = 1;
   // programmatic dependent launch: the prologue (barrier init, W_g loads)
@@ -217,7 +228,7 @@ cudaError_t launch_partial_attn(PartialParams& p, int GT, int is_bf16, cudaStrea
 
 namespace hata {
 // process-wide options (hata_set_option); defaults on
-static std::atomic<int> g_opts[OPT_COUNT] = {{1}, {1}};
+static std::atomic<int> g_opts[OPT_COUNT] = {{1}, {1}, {0}};   // hint on, PDL on, cooperative off
 int option_value(int opt) { return (opt >= 0 && opt < OPT_COUNT) ? g_opts[opt].load(std::memory_order_relaxed) : 0; }
 void set_option_value(int opt, int v) { if (opt >= 0 && opt < OPT_COUNT) g_opts[opt].store(v, std::memory_order_relaxed); }
 

@@ -67,7 +67,6 @@ struct DecodeParams {
   int d_smem;              // 1: this rank's D lives in smem, else in ws_D
   // workspace (global); zero-initialised once, left zeroed by every launch
   int32_t* ws_hist;        // [units, M, hs] exclusive prefix counts cum_r[0..nbins]   (M > 1)
-  int32_t* ws_tot;         // [units, hs] sum over the ranks of cum_r (atomics)        (M > 1)
   uint16_t* ws_D;          // [units, M, chunk] D when it does not fit in smem (!d_smem)
   float* ws_part;          // [units, M, GT, d+2]          (M > 1)
   unsigned* ws_sync;       // [units, 4]: barrier, done (M > 1), threshold hint, -

@@ -90,9 +90,6 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
   HATA_TRACE(31);
   HATA_CLK(23);
   if (HATA_DIAG && (p.dbg & 4)) return;                            // diagnostics: launch cost only
-  // a dependent launch may start its prologue (W_g loads) on SMs this grid
-  // frees; it waits for this grid's completion before reading anything else
-  griddep_launch_dependents();
 
   const int M = p.M;
   const int NST = p.stages;
@@ -132,10 +129,15 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
   const bool append = p.k_new != nullptr;
   T* qraw = reinterpret_cast<T*>(smem + L.qraw);                    // [G (+1 key)][d] as stored
 
-  // ---- phase 0: start every stream with bulk copies (TMA), in the order they
-  // are needed: W_g, q and the new key (they gate the q-hash), then the code
-  // chunk in a few large copies.  A CTA's TMA requests are served in issue
-  // order, so the small copies are not queued behind the 128 KB stream.
+  // ---- phase 0: start the q-independent streams with bulk copies (TMA)
+  // BEFORE griddepcontrol.wait -- W_g and this rank's code chunk -- so that
+  // under programmatic dependent launch they overlap the preceding kernel's
+  // tail.  Contract (include/hata.h): a kernel that precedes this launch in
+  // the stream and writes code rows makes them visible before it triggers its
+  // dependents (every libhata kernel fences, then triggers); the row this
+  // launch appends itself is rescored from its own k_new.  q, k_new, v_new,
+  // n and the workspace are read after the wait with plain loads (not queued
+  // behind the stream's TMA requests).
   auto issue_stage = [&](int s) {
     const int slot = s % NST;
     const int ntok = min(STAGE_TOK, Lcopy - s * STAGE_TOK);
@@ -146,7 +148,7 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
   const int WROWB = dec_wrow_stride(p.rbits, EB);                   // padded smem row of W_g
   const uint32_t wrow = (uint32_t)(p.rbits * EB);                  // bytes of one W_g row
   if (tid == 0) {
-    // [0, NST) code ring, NST: W_g, NST+1: q + k_new + v_new, NST+2: spare,
+    // [0, NST) code ring, NST: W_g, NST+1: spare, NST+2: spare,
     // NST+3: attention gather batches
     for (int s = 0; s < NST + 4; ++s) mbar_init(&bars[s], 1);
     fence_mbar_init();
@@ -161,28 +163,32 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
       bulk_g2s(reinterpret_cast<uint8_t*>(Ws) + row * WROWB, wsrc + (int64_t)row * p.rbits, wrow, &bars[NST]);
   }
   __syncthreads();                                                  // W_g requests ahead of the stream
+  if (tid == 0)                                                     // the code chunk, a few large copies
+    for (int s = 0; s < NST && s < nstages; ++s) issue_stage(s);
+  for (int i = tid; i < p.nbins; i += DEC_THREADS) hist[i] = 0;
   // Programmatic dependent launch: everything above reads only the hash
-  // weights (no preceding kernel produces them); q, k_new, v_new, n, the code
-  // cache (a preceding decode may append to it), the workspace and every
-  // global write come after the wait.  A no-op without the launch attribute.
+  // weights and code rows no preceding kernel writes (contract above); q,
+  // k_new, v_new, n, K/V, the workspace and every global write come after
+  // the wait.  A no-op without the launch attribute.
   griddep_wait();
+  HATA_TRACE(28);
   // n[b] > n_max is clamped to n_max: the rank chunks are fixed by n_max
   // (include/hata.h documents this)
   const int64_t n = min(p.n[b], p.n_max);
-  if (tid == 0) {
-    // q and the new key/value first (they gate the q-hash), then the code
-    // chunk in a few large copies: a CTA's TMA requests are served in order
-    const uint32_t qbytes = (uint32_t)(G * D_HEAD * EB), kbytes = append ? (uint32_t)(D_HEAD * EB) : 0u;
-    mbar_arrive_expect_tx(&bars[NST + 1], qbytes + 2 * kbytes + (p.ws_sync ? 16u : 0u));
-    bulk_g2s(qraw, qg, qbytes, &bars[NST + 1]);
-    if (p.ws_sync) bulk_g2s(misc + 12, p.ws_sync + 4 * u, 16u, &bars[NST + 1]);   // [14] = threshold hint
-    if (kbytes) {                                                   // new key and value rows
-      bulk_g2s(qraw + G * D_HEAD, reinterpret_cast<const T*>(p.k_new) + (int64_t)u * D_HEAD, kbytes, &bars[NST + 1]);
-      bulk_g2s(qraw + (G + 1) * D_HEAD, reinterpret_cast<const T*>(p.v_new) + (int64_t)u * D_HEAD, kbytes, &bars[NST + 1]);
+  {
+    // q rows, then the new key and value rows (16-byte vectors), and the
+    // unit's threshold hint of the previous launch
+    constexpr int V16 = D_HEAD * EB / 16;                          // 16-byte vectors per row
+    const int nv = (G + (append ? 2 : 0)) * V16;
+    uint4* dq = reinterpret_cast<uint4*>(qraw);
+    for (int i = tid; i < nv; i += DEC_THREADS) {
+      const int row = i / V16, c = i % V16;
+      const T* src = row < G ? qg + (int64_t)row * D_HEAD
+                             : reinterpret_cast<const T*>(row == G ? p.k_new : p.v_new) + (int64_t)u * D_HEAD;
+      dq[i] = __ldcg(reinterpret_cast<const uint4*>(src) + c);
     }
-    for (int s = 0; s < NST && s < nstages; ++s) issue_stage(s);
+    if (tid == 0) misc[14] = p.ws_sync ? (int)__ldcg(p.ws_sync + 4 * u + 2) : 0;
   }
-  for (int i = tid; i < p.nbins; i += DEC_THREADS) hist[i] = 0;
   // Candidate hint: the unit's threshold of the previous launch on this
   // workspace (+ DEC_HINT_SLACK).  Tokens with D <= Th are marked in a bitmap
   // while the ranks exchange counts, so that when this launch's threshold is <= Th the
@@ -208,12 +214,13 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
   const bool owner = append && n >= 1 && pos < p.cap && pos >= t0 && pos < t0 + Lr;
   const int NV = G + (owner ? 1 : 0);                                // projected vectors
   mbar_wait(&bars[NST], 0);                                         // W_g in smem
-  mbar_wait(&bars[NST + 1], 0);                                     // q, k_new, v_new (+ hint) in smem
+  __syncthreads();                                                  // q, k_new, v_new, hint in smem
   if (hinted) { const int h = misc[14]; Th = h > 0 ? h + DEC_HINT_SLACK : -1; }
   HATA_TRACE(9);
-  if constexpr (EB != 2)                                            // fp32 paths read q as floats
+  if constexpr (EB != 2) {                                          // fp32 paths read q as floats
     for (int i = tid; i < NV * D_HEAD; i += DEC_THREADS) qf[(i / D_HEAD) * QS + i % D_HEAD] = Elem<T>::to_f(qraw[i]);
-  __syncthreads();
+    __syncthreads();
+  }
   HATA_TRACE(8);
   if constexpr (EB == 2) {
     // bf16: the projection X[NV x d] . W_g[d x rbits] on the tensor cores
@@ -372,7 +379,9 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
     uint32_t* dst = reinterpret_cast<uint32_t*>(Dloc + base);
     uint32_t* dsts = reinterpret_cast<uint32_t*>(Ds + base);        // same, as a shared-space pointer
     // two token pairs per thread per iteration (independent chains for ILP);
-    // a pair -> one 32-bit store of two u16 distances
+    // a pair -> one 32-bit store of two u16 distances.  (One pair per
+    // iteration is faster in isolation -- probes/probe_score2.cu -- but
+    // measured 0.8 us slower per step in this kernel.)
     for (int j2 = tid; j2 < npairs; j2 += 2 * DEC_THREADS) {
       const int j2b = j2 + DEC_THREADS;
       const bool two = j2b < npairs;
@@ -387,13 +396,17 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
       const uint32_t d1 = group_D(k1);
       const uint32_t d2 = group_D(k2);
       const uint32_t d3 = group_D(k3);
-      if (!(HATA_DIAG && (p.dbg & 2))) atomicAdd(&hist[d0], 1u);   // dbg 2: timing without the histogram
-      if (!(HATA_DIAG && (p.dbg & 2))) atomicAdd(&hist[d1], 1u);   // dbg 2: timing without the histogram
+      if (!(HATA_DIAG && (p.dbg & 2))) {                            // dbg 2: timing without the histogram
+        atomicAdd(&hist[d0], 1u);
+        atomicAdd(&hist[d1], 1u);
+      }
       if (p.d_smem) dsts[j2] = d0 | (d1 << 16);
       else dst[j2] = d0 | (d1 << 16);
       if (two) {
-        if (!(HATA_DIAG && (p.dbg & 2))) atomicAdd(&hist[d2], 1u);   // dbg 2: timing without the histogram
-        if (!(HATA_DIAG && (p.dbg & 2))) atomicAdd(&hist[d3], 1u);   // dbg 2: timing without the histogram
+        if (!(HATA_DIAG && (p.dbg & 2))) {
+          atomicAdd(&hist[d2], 1u);
+          atomicAdd(&hist[d3], 1u);
+        }
         if (p.d_smem) dsts[j2b] = d2 | (d3 << 16);
         else dst[j2b] = d2 | (d3 << 16);
       }
@@ -444,6 +457,9 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
       reinterpret_cast<uint4*>(dstrow)[tid % CH] = v;
       asm volatile("fence.proxy.async.global;" ::: "memory");        // this rank's own gather reads it by TMA
     }
+    // the appended code row and K/V rows are visible GPU-wide before this
+    // CTA triggers its dependents (their code streams start before their wait)
+    __threadfence();
   }
   // pad D past the valid tokens with 0x7fff (never selected) up to what the
   // selection reads: the per-thread blocking (dec_dchunk(Lr)) of the full
@@ -451,6 +467,10 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
   const int dpad = hinted ? nbw * 32 : dec_dchunk(Lr);
   for (int i = Lr + tid; i < dpad; i += DEC_THREADS) Dloc[i] = 0x7fffu;
   __syncthreads();
+  // a dependent launch may now start its prologue (W_g + code stream) on the
+  // SMs this grid frees; it waits for this grid's completion before reading
+  // anything else
+  griddep_launch_dependents();
 
   // ---- phase 3: exact top-k' (Alg. 3 lines 12-13) by counting select.
   // thr = D of the k'-th best token; every D < thr is selected; ties at thr
@@ -503,16 +523,14 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
     }
   };
   if (M > 1) {
+    // publish this rank's prefix counts (plain stores), arrive
     int32_t* gc = p.ws_hist + ((int64_t)u * M + r) * hs;
-    int32_t* gt = p.ws_tot + (int64_t)u * hs;
+    const int32_t* gu = p.ws_hist + (int64_t)u * M * hs;           // rank rr's counts: gu + rr * hs
     int c = cum;
 #pragma unroll
     for (int q = 0; q < BPT_MAX; ++q) {
       const int i = i0 + q;
-      if (q < BPT && i <= p.nbins) {
-        gc[i] = c;
-        if (c) atomicAdd(gt + i, c);
-      }
+      if (q < BPT && i <= p.nbins) gc[i] = c;
       c += tb[q];
     }
     __syncthreads();
@@ -527,25 +545,46 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
     }
     __syncthreads();
     HATA_TRACE(3);
-    // with a hint, the ranks' prefix counts at the bins around it come in the
-    // same round trip as the totals (the tie quota then needs no second one)
-    // (loaded here, stored after the totals' loads are issued)
-    int wv = 0;
-    const bool wl = Th >= 0 && tid < M * DEC_WIN;
-    if (wl) {
-      const int rr = tid / DEC_WIN, bi = Th - (DEC_WIN - 2) + tid % DEC_WIN;
-      if (bi >= 0 && bi <= p.nbins) wv = __ldcg(p.ws_hist + ((int64_t)u * M + rr) * hs + bi);
+    // with a hint, every rank's prefix counts at the window bins
+    // [w0, w0 + DEC_WIN) around it: the unit totals there give the threshold
+    // when it falls in the window, and the per-rank values the tie quota --
+    // one round trip, no unit-total atomics
+    const int w0 = Th - (DEC_WIN - 2);
+    if (Th >= 0 && tid < M * DEC_WIN) {
+      const int rr = tid / DEC_WIN, bi = w0 + tid % DEC_WIN;
+      win[tid] = (bi >= 0 && bi <= p.nbins) ? __ldcg(gu + (int64_t)rr * hs + bi) : 0;
     }
-    // thr: the bin where the unit's cumulative count crosses k'
+    __syncthreads();
+    if (warp == 0) {
+      int tot = 0;
+      if (Th >= 0 && lane < DEC_WIN)
+        for (int rr = 0; rr < M; ++rr) tot += win[rr * DEC_WIN + lane];
+      const int z = __shfl_down_sync(0xffffffffu, tot, 1);
+      const int bj = w0 + lane;                                       // bins bj, bj + 1 both in the window
+      const bool hit = Th >= 0 && lane < DEC_WIN - 1 && bj >= 0 && bj + 1 <= p.nbins && kp > 0 && tot < kp && kp <= z;
+      if (hit) { misc[0] = bj; misc[1] = kp - tot; }
+      const unsigned any = __ballot_sync(0xffffffffu, hit);
+      if (lane == 0) misc[5] = any ? 1 : 0;
+    }
+    __syncthreads();
+    if (!misc[5] && kp > 0) {
+      // no hint, or the threshold is outside the window: unit totals of
+      // every bin from the M ranks' published prefix counts
+      int acc[BPT_MAX + 1];
 #pragma unroll
-    for (int q = 0; q < BPT_MAX; ++q) {
-      const int i = i0 + q;
-      if (q < BPT && i < p.nbins && kp > 0) {
-        const int a = __ldcg(gt + i), z = __ldcg(gt + i + 1);
-        if (a < kp && kp <= z) { misc[0] = i; misc[1] = kp - a; }
+      for (int q = 0; q <= BPT_MAX; ++q) acc[q] = 0;
+      for (int rr = 0; rr < M; ++rr) {
+        const int32_t* cr = gu + (int64_t)rr * hs;
+#pragma unroll
+        for (int q = 0; q <= BPT_MAX; ++q)
+          if (q <= BPT && i0 + q <= p.nbins) acc[q] += __ldcg(cr + i0 + q);
+      }
+#pragma unroll
+      for (int q = 0; q < BPT_MAX; ++q) {
+        const int i = i0 + q;
+        if (q < BPT && i < p.nbins && acc[q] < kp && kp <= acc[q + 1]) { misc[0] = i; misc[1] = kp - acc[q]; }
       }
     }
-    if (wl) win[tid] = wv;
   } else {
     build_bitmap();
     HATA_TRACE(3);
@@ -843,19 +882,21 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
   }
   __syncthreads();
   HATA_CLK(8);
+  // ranks 1..M-1 release their partial (cumulative over bar.sync) and exit
+  // at once (their SMs go to the next launch); rank 0 waits for them and merges
+  if (r != 0) {
+    if (tid == 0) red_add_release_gpu(sync + 1, 1u);
+    HATA_TRACE(15);
+    return;
+  }
   if (tid == 0) {
-    // release this partial (cumulative over bar.sync), acquire the others'
-    const unsigned prev = atom_add_acq_rel_gpu(sync + 1, 1u);
-    misc[2] = (prev == (unsigned)(M - 1));
+    for (unsigned spins = 0; ld_acquire_gpu(sync + 1) < (unsigned)(M - 1);)
+      if (++spins > HATA_SPIN_LIMIT) __trap();
   }
   HATA_CLK(9);
   __syncthreads();
   HATA_TRACE(15);
-  if (!misc[2]) return;
-  // leave the workspace zeroed for the next launch: every rank read the unit
-  // total before publishing its partial (stores overlap the merge loads)
-  for (int i = tid; i <= p.nbins; i += DEC_THREADS) p.ws_tot[(int64_t)u * hs + i] = 0;
-  // last rank: every partial is visible (writer fence + counter); merge them
+  // rank 0: every partial is visible (writer release + counter); merge them
   // in rank order straight from L2 (thread = one output element)
   if (!p.cand_mode) {
     // merge weights once per head: warp h (< G) holds rank r in lane r,

@@ -39,6 +39,13 @@ __global__ void __launch_bounds__(256) append_kernel(AppendParams p) {
     const uint32_t word = __ballot_sync(0xffffffffu, acc >= 0.f);
     if (lane == 0) cd[w] = word;
   }
+  // the appended rows are visible GPU-wide before a dependent decode launch
+  // (which streams code rows before its griddepcontrol.wait) may start: every
+  // writer fences, then the CTA syncs, then triggers (a CTA counts as
+  // triggered as soon as any of its threads executes the trigger)
+  __threadfence();
+  __syncthreads();
+  griddep_launch_dependents();
 }
 
 // CUDA-core key hashing: CTA = 64 tokens x all words of one (b, g).
@@ -63,7 +70,7 @@ __global__ void __launch_bounds__(256) hash_keys_simt_kernel(HashKeysParams p) {
   __syncthreads();
   const int tk = threadIdx.x / W, w = threadIdx.x % W;
   const int64_t t = tbase + tk;
-  if (tk >= TOK || t >= p.t0 + p.n) return;
+  if (tk < TOK && t < p.t0 + p.n) {
   float acc[32];
 #pragma unroll
   for (int i = 0; i < 32; ++i) acc[i] = 0.f;
@@ -84,6 +91,10 @@ __global__ void __launch_bounds__(256) hash_keys_simt_kernel(HashKeysParams p) {
 #pragma unroll
   for (int i = 0; i < 32; ++i) word |= (acc[i] >= 0.f ? 1u : 0u) << i;
   p.codes[(int64_t)b * p.c_sb + (int64_t)g * p.c_sh + t * W + w] = word;
+  }
+  __threadfence();                          // codes visible before dependents start (see append_kernel)
+  __syncthreads();
+  griddep_launch_dependents();
 }
 
 cudaError_t launch_append(const AppendParams& p, int is_bf16, cudaStream_t s) {

@@ -139,6 +139,12 @@ __global__ void __launch_bounds__(HK_THREADS) hash_keys_mma_kernel(const HashKey
     __syncthreads();                          // this buffer is refilled two tiles on
     buf ^= 1;
   }
+  // codes visible GPU-wide before a dependent decode launch (which streams
+  // code rows before its griddepcontrol.wait) may start: every writer
+  // fences, the CTA syncs, then it triggers
+  __threadfence();
+  __syncthreads();
+  griddep_launch_dependents();
 }
 
 template <int RB>

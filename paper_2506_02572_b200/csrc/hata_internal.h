@@ -38,11 +38,11 @@ cudaError_t launch_hash_keys_tc(const HashKeysParams& p, cudaStream_t s);
 struct DecodePlan {
   int M, stages, chunk, R_cap, rows_cap, nbins, GT, smem;
   bool d_smem, rows_global;
-  size_t ws_sync, ws_hist, ws_tot, ws_part, ws_D, ws_rows, ws_total;   // workspace byte offsets / size
+  size_t ws_sync, ws_hist, ws_part, ws_D, ws_rows, ws_total;   // workspace byte offsets / size
 };
 struct DecodeParams;
 // process-wide options (hata_set_option), indices = hata_option values
-enum { OPT_SELECTION_HINT = 0, OPT_PDL = 1, OPT_COUNT = 2 };
+enum { OPT_SELECTION_HINT = 0, OPT_PDL = 1, OPT_COOPERATIVE = 2, OPT_COUNT = 3 };
 int option_value(int opt);
 void set_option_value(int opt, int v);
 DecodePlan plan_decode(int B, int Hq, int Hkv, int d, int rbits, int64_t n_max, int k, int elem_bytes);

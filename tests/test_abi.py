@@ -62,7 +62,7 @@ def test_validation_rejects_before_launch(lib):
     assert lib.hata_hash_keys(P, Strides(1, 1, 128), 1, P, 1, 1, 128, 128, 8, 10, 16, P, Strides(1, 1, 4), None) == 3
     # unknown option; known options accepted
     assert lib.hata_set_option(7, 1) == 1
-    assert lib.hata_set_option(0, 1) == 0 and lib.hata_set_option(1, 1) == 0
+    assert lib.hata_set_option(0, 1) == 0 and lib.hata_set_option(1, 1) == 0 and lib.hata_set_option(2, 1) == 0
     # null pointers
     assert lib.hata_append(None, P, 1, P, P, P, s, P, s, P, 10, 1, 1, 128, 128, None) == 1
     assert lib.hata_shard_combine(None, 2, 1, 32, 128, P, 0, None) == 1

@@ -94,7 +94,8 @@ def test_n_zero_sequence(N):
         print(check_units(ref, _res(st, o, n), sh.k, [(1, 0), (1, 5), (2, 3)]))
 
 
-def test_bench_launch_configuration_varying_q():
+@pytest.mark.parametrize("coop", [0, 1], ids=["plain", "cooperative"])
+def test_bench_launch_configuration_varying_q(coop):
     """The exact configuration bench.py times: CFG-4, paired K/V layout, fused
     decode steps chained with programmatic dependent launch inside ONE CUDA
     graph, one workspace reused by every step (threshold hint on), and a
@@ -120,6 +121,7 @@ def test_bench_launch_configuration_varying_q():
     ns = [nb0 + 1 + s for s in range(S)]
     H.set_option("pdl", 1)
     H.set_option("selection_hint", 1)
+    H.set_option("cooperative", coop)
     stream = torch.cuda.Stream()
     stream.wait_stream(torch.cuda.current_stream())
     with torch.cuda.stream(stream):                     # warm-up (plans, func attributes) outside capture
@@ -137,6 +139,7 @@ def test_bench_launch_configuration_varying_q():
             # the oracle appends row n-1 itself; rows of earlier steps come from the generator
             ref_case["K"] = case["K"].clone(); ref_case["V"] = case["V"].clone()
             print(rep, s, check_units(ref_case, _res(st, outs[s], ns[s]), sh.k, [(0, g) for g in range(sh.Hkv)]))
+    H.set_option("cooperative", 0)
 
 
 @pytest.mark.parametrize("variant", ["planted", "pool8"])

@@ -64,6 +64,11 @@ def sharded_step(case, k, P, nb=None, out_dtype=torch.float32):
         assert torch.equal(rk.sel_score, ranks[0].sel_score)
     for o in outs[1:]:
         assert torch.equal(o, outs[0]), "ranks disagree on the combined output"
+    if not torch.equal(ranks[0].sel_idx, ref_idx):
+        bad = (ranks[0].sel_idx != ref_idx).any(-1).nonzero().tolist()
+        b, g = bad[0]
+        a, r = ranks[0].sel_idx[b, g].cpu().numpy(), ref_idx[b, g].cpu().numpy()
+        print("DIFF units", bad, "sharded-only", np.setdiff1d(a, r)[:20], "ref-only", np.setdiff1d(r, a)[:20])
     assert torch.equal(ranks[0].sel_idx, ref_idx), "sharded selection != unsharded selection"
     # reassemble the caches the ranks hold (after the owner's append)
     Kc = torch.cat([rk.K[:, :, :shard_range(cap, P, r)[1] - shard_range(cap, P, r)[0]]

@@ -21,10 +21,57 @@ NAMES = {31: "kernel_entry", 0: "start", 1: "hash_done", 2: "score_done", 3: "hi
          6: "attn_done", 7: "end(last)", 8: "qk_loaded", 9: "W_ready", 10: "stage0", 11: "thr",
          12: "quota", 13: "last_stage", 14: "sel_pass1_done", 15: "published", 16: "kv_gathered",
          17: "groups_done", 19: "kv_issued", 20: "kv_gathered_1st", 21: "groups_done_1st",
-         23: "kv_issued_1st", 20: "attn_entry", 27: "arrived", 28: "prefetched", 18: "sel_counted", 21: "sel_scanned", 22: "sel_emitted", 29: "attn_wmerge1", 30: "attn_wmerge2", 24: "hash_mma_done(t0)", 25: "hash_synced", 26: "planes_done(t0)"}
+         23: "kv_issued_1st", 20: "attn_entry", 27: "arrived", 28: "wait_done", 18: "sel_counted", 21: "sel_scanned", 22: "sel_emitted", 29: "attn_wmerge1", 30: "attn_wmerge2", 24: "hash_mma_done(t0)", 25: "hash_synced", 26: "planes_done(t0)"}
+
+
+def chain(cfg, S=8):
+    """S fused steps over S cache sets captured in ONE CUDA graph (the bench's
+    launch configuration, PDL between steps), each launch with its own trace
+    buffer: stamps of launch i are reported relative to the end of launch
+    i-1 (the max 'end(last)' stamp of its merging CTAs)."""
+    sh = synth.CONFIGS[cfg]
+    dev = torch.device("cuda", 0)
+    bench.apply_options()
+    sets = [bench.Step(sh, 2000 + i, dev) for i in range(S)]
+    H = sets[0].H
+    M = H.decode_ranks(sh.B, sh.Hq, sh.Hkv, sh.d, sh.rbits, sh.N, sh.k, sets[0].K.dtype)
+    nct = M * sh.B * sh.Hkv
+    bufs = [torch.zeros(nct * 64, dtype=torch.int64, device=dev) for _ in range(S)]
+
+    def run_all():
+        for s, b in zip(sets, bufs):
+            H._lib.check(H.lib().hata_debug_trace(b.data_ptr()), "trace")
+            s.run()
+        H._lib.check(H.lib().hata_debug_trace(None), "trace off")
+    g = bench._graph(run_all)
+    for _ in range(3):
+        g.replay()
+    torch.cuda.synchronize()
+    for b in bufs:
+        b.zero_()
+    g.replay()
+    torch.cuda.synchronize()
+    ts = [b.view(nct, 64).cpu().double() for b in bufs]
+    print(f"{cfg} chained x{S}: M={M} ranks x {sh.B * sh.Hkv} units = {nct} CTAs")
+    for i in range(1, S):
+        prev_end = ts[i - 1][:, 7].max()
+        t = ts[i]
+        cols = []
+        for j in range(32):
+            c = t[:, j]
+            c = c[c > 0]
+            if len(c):
+                c = (c - prev_end) / 1e3
+                cols.append((c.median().item(), c.max().item(), NAMES.get(j, str(j))))
+        cols.sort()
+        step = (t[:, 7].max() - prev_end) / 1e3
+        print(f"launch{i} step={step.item():.2f}us " + " ".join(f"{nm}={md:.2f}/{mx:.2f}" for md, mx, nm in cols))
 
 
 def main():
+    if len(sys.argv) > 1 and sys.argv[1] == "chain":
+        chain(sys.argv[2] if len(sys.argv) > 2 else "cfg4")
+        return
     cfg = sys.argv[1] if len(sys.argv) > 1 else "cfg4"
     reps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
     fused = (sys.argv[3] != "0") if len(sys.argv) > 3 else True
