@@ -273,7 +273,7 @@ def bench_hash_keys(st, reps):
     kbytes = sh.B * sh.Hkv * n * sh.d * eb
     flops = 2.0 * sh.B * sh.Hkv * n * sh.d * sh.rbits
     return {"us": us, "keys": sh.B * sh.Hkv * n, "GBps_K_read": kbytes / (us * 1e-6) / 1e9,
-            "TFLOPs": flops / (us * 1e-6) / 1e12, "kernel": "hash_keys_mma_kernel (mma.sync bf16, fp32 acc)",
+            "TFLOPs": flops / (us * 1e-6) / 1e12, "kernel": "hash_keys_umma_kernel (tcgen05.mma kind::f16, TMEM fp32 accumulators, TMA SW128 K tiles)",
             "note": "cache resident from the previous call (L2 holds at most 126 MB of the K read)"}
 
 

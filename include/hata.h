@@ -72,9 +72,11 @@ typedef struct CUstream_st* hata_stream_t; /* == cudaStream_t */
  *   codes   output rows [t0, t0 + n) of [B, H_kv, cap, rbits/32] (strides cs).
  *   cap     rows allocated per (b, KV head) in K and codes; t0 + n > cap ->
  *           CAPACITY (nothing enqueued).
- * bf16 inputs run on the tensor cores (mma.sync m16n8k16 HMMA, exact bf16
- * products, fp32 accumulation, sign-pack epilogue); fp32 inputs run on CUDA
- * cores (fp32 FMA).
+ * bf16 inputs run on the 5th-generation tensor cores: K tiles by TMA
+ * (128-byte swizzle), tcgen05.mma with fp32 accumulation in TMEM, W resident
+ * in shared memory, tcgen05.ld sign-pack epilogue -- when one 2-D tensor map
+ * covers K (its b and h strides are multiples of its row stride), otherwise
+ * mma.sync (HMMA); fp32 inputs run on CUDA cores (fp32 FMA).
  * Errors: INVALID_ARG (null pointers, n < 0, rbits % 32, strides),
  *         CAPACITY, UNSUPPORTED (d, rbits, dtype), CUDA.
  * ------------------------------------------------------------------------ */

@@ -28,7 +28,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
          "-Xptxas", "-v", "-I", INCLUDE, "-I", CSRC] + (["-DHATA_TRACE_ENABLED=1"] if TRACE else []) + DEFS
-SOURCES = ["hata_abi.cu", "hata_decode.cu", "hata_hash.cu", "hata_hash_tc.cu", "hata_shard.cu"]
+SOURCES = ["hata_abi.cu", "hata_decode.cu", "hata_hash.cu", "hata_hash_tc.cu", "hata_hash_umma.cu", "hata_shard.cu"]
 
 
 def _deps():

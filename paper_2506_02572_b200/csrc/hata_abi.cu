@@ -121,10 +121,12 @@ hata_status hata_hash_keys(const void* K, hata_strides ks, hata_dtype dt, const 
   hata::HashKeysParams p = {};
   p.K = K; p.kv_sb = ks.sb; p.kv_sh = ks.sh; p.kv_st = ks.st;
   p.Wh = W; p.codes = codes; p.c_sb = cs.sb; p.c_sh = cs.sh;
-  p.t0 = t0; p.n = n; p.B = B; p.Hkv = H_kv; p.d = d; p.rbits = rbits;
+  p.t0 = t0; p.n = n; p.cap = cap; p.B = B; p.Hkv = H_kv; p.d = d; p.rbits = rbits;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   if (dt == HATA_BF16) {
-    cudaError_t e = hata::launch_hash_keys_tc(p, s);
+    cudaError_t e = hata::launch_hash_keys_umma(p, s);         // tcgen05 + TMEM + TMA
+    if (e != cudaErrorNotSupported) return cuda_status(e);
+    e = hata::launch_hash_keys_tc(p, s);                       // strides no tensor map covers: mma.sync
     if (e != cudaErrorNotSupported) return cuda_status(e);
   }
   return cuda_status(hata::launch_hash_keys_simt(p, dt == HATA_BF16, s));

@@ -27,12 +27,16 @@ struct HashKeysParams {
   uint32_t* codes;
   int64_t c_sb, c_sh;
   int64_t t0, n;       // rows [t0, t0 + n) of every (b, g)
+  int64_t cap;         // rows allocated per (b, g) (extent of the TMA tensor map)
   int B, Hkv, d, rbits;
 };
 
 cudaError_t launch_append(const AppendParams& p, int is_bf16, cudaStream_t s);
 cudaError_t launch_hash_keys_simt(const HashKeysParams& p, int is_bf16, cudaStream_t s);
-// tcgen05 path (bf16, d == 128, rbits in {128, 256}); returns cudaErrorNotSupported otherwise.
+// tcgen05/TMEM/TMA path (bf16, d == 128, rbits in {32, 64, 128, 256}, K strides
+// that one 2-D tensor map covers); cudaErrorNotSupported otherwise.
+cudaError_t launch_hash_keys_umma(const HashKeysParams& p, cudaStream_t s);
+// legacy tensor-core path (mma.sync, bf16, d == 128): any strides.
 cudaError_t launch_hash_keys_tc(const HashKeysParams& p, cudaStream_t s);
 
 struct DecodePlan {
