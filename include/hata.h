@@ -208,22 +208,29 @@ hata_status hata_shard_candidates(const void* q, hata_dtype dt, const uint32_t* 
                                   int32_t* cand_idx, void* workspace, size_t ws_bytes, hata_stream_t stream);
 
 /* Phase 2: global merge.  all_D / all_idx are the P ranks' candidate lists
- * gathered rank-major: [P, B, H_kv, k].  Selects the global k' = min(k, n_total[b])
+ * gathered rank-major: rank r's [B, H_kv, k] block starts rank_stride
+ * elements after rank r-1's (0 = B*H_kv*k, i.e. [P, B, H_kv, k]; a packed
+ * per-rank [D | idx] buffer gathered with one collective uses 2*B*H_kv*k).
+ * Selects the global k' = min(k, n_total[b])
  * smallest (D, index) pairs (identical on every rank) and returns those that
  * fall in [lo, hi) as LOCAL indices (global - lo), ascending, in own_idx
  * [B, H_kv, k] (-1 padding) with counts own_cnt [B, H_kv].  Optionally the
  * whole global selection (ascending) in sel_idx [B, H_kv, k] and its S values
  * in sel_score.  n_total: DEVICE int64 [B]. */
-hata_status hata_shard_select(const int32_t* all_D, const int32_t* all_idx, int P, int B, int H_kv, int k, int G,
-                              int rbits, const int64_t* n_total, int64_t lo, int64_t hi, int32_t* own_idx,
-                              int32_t* own_cnt, int32_t* sel_idx, int32_t* sel_score, hata_stream_t stream);
+hata_status hata_shard_select(const int32_t* all_D, const int32_t* all_idx, int64_t rank_stride, int P, int B,
+                              int H_kv, int k, int G, int rbits, const int64_t* n_total, int64_t lo, int64_t hi,
+                              int32_t* own_idx, int32_t* own_cnt, int32_t* sel_idx, int32_t* sel_score,
+                              hata_stream_t stream);
 
-/* Phase 3: partial attention over own selected rows.
- *   partial [B, H_q, d + 2] fp32: (m, l, acc[d]) with m = max logit,
- *   l = sum exp(z - m), acc = sum exp(z - m) V  (flash-decoding partials). */
+/* Phase 3: partial attention over own selected rows, split over `splits`
+ * CTAs per (b, KV head) (split s takes rows [s*cnt/S, (s+1)*cnt/S) of the
+ * ascending own list; bf16 on the tensor cores, gather fused).
+ *   partial [splits, B, H_q, d + 2] fp32: (m, l, acc[d]) with m = max logit
+ *   (-inf for an empty split), l = sum exp(z - m), acc = sum exp(z - m) V
+ *   (flash-decoding partials; a rank's splits combine like extra ranks). */
 hata_status hata_shard_partial_attn(const void* q, const void* K, const void* V, hata_strides kvs, hata_dtype dt,
                                     const int32_t* own_idx, const int32_t* own_cnt, int B, int H_q, int H_kv, int d,
-                                    int k, float scale, float* partial, hata_stream_t stream);
+                                    int k, float scale, int splits, float* partial, hata_stream_t stream);
 
 /* Phase 4: combine P partials gathered rank-major [P, B, H_q, d + 2] in rank
  * order (deterministic): M = max m_r, L = sum l_r e^{m_r - M},

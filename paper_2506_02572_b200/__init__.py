@@ -171,21 +171,27 @@ def shard_candidates(q, codes, W, n_local, n_local_max: int, token_offset: int, 
 
 def shard_select(all_D, all_idx, n_total, lo: int, hi: int, G: int, rbits: int, own_idx, own_cnt, sel_idx=None,
                  sel_score=None, stream=None):
+    """all_D / all_idx: [P, B, H_kv, k] views whose rank blocks may be strided
+    (e.g. the two halves of one gathered [P, 2, B, H_kv, k] buffer)."""
     _need_cuda(all_D, all_idx, n_total, own_idx, own_cnt)
     P, B, Hkv, k = all_D.shape
-    _lib.check(lib().hata_shard_select(_p(all_D), _p(all_idx), P, B, Hkv, k, G, rbits, _p(n_total), lo, hi,
-                                       _p(own_idx), _p(own_cnt), _p(sel_idx), _p(sel_score), _stream(stream)),
-               "hata_shard_select")
+    if all_D.stride()[1:] != (Hkv * k, k, 1) or all_idx.stride() != all_D.stride():
+        raise HataError("candidate blocks must be [B, H_kv, k] contiguous with one rank stride")
+    _lib.check(lib().hata_shard_select(_p(all_D), _p(all_idx), all_D.stride(0), P, B, Hkv, k, G, rbits,
+                                       _p(n_total), lo, hi, _p(own_idx), _p(own_cnt), _p(sel_idx), _p(sel_score),
+                                       _stream(stream)), "hata_shard_select")
 
 
 def shard_partial_attn(q, K, V, own_idx, own_cnt, k: int, partial, scale: float = 0.0, stream=None):
+    """partial: [splits, B, H_q, d + 2] fp32 (splits CTAs per (b, KV head))."""
     _need_cuda(q, K, V, own_idx, own_cnt, partial)
     q = q.contiguous()
     B, Hq, d = q.shape
     Hkv = K.shape[1]
+    splits = partial.shape[0] if partial.dim() == 4 else 1
     _lib.check(lib().hata_shard_partial_attn(_p(q), _p(K), _p(V), _strides4(K), _dt(K), _p(own_idx),
-                                             _p(own_cnt), B, Hq, Hkv, d, k, scale, _p(partial), _stream(stream)),
-               "hata_shard_partial_attn")
+                                             _p(own_cnt), B, Hq, Hkv, d, k, scale, splits, _p(partial),
+                                             _stream(stream)), "hata_shard_partial_attn")
 
 
 def shard_combine(partials, out, stream=None):

@@ -46,10 +46,10 @@ _SIGS = {
     "hata_decode_ranks": (c_i32, [c_i32, c_i32, c_i32, c_i32, c_i32, c_i64, c_i32, c_i32]),
     "hata_shard_candidates": (c_i32, [c_ptr, c_i32, c_ptr, Strides, c_ptr, c_i32, c_i32, c_i32, c_i32, c_i32, c_ptr,
                                       c_i64, c_i64, c_i32, c_ptr, c_ptr, c_ptr, c_size, c_ptr]),
-    "hata_shard_select": (c_i32, [c_ptr, c_ptr, c_i32, c_i32, c_i32, c_i32, c_i32, c_i32, c_ptr, c_i64, c_i64,
-                                  c_ptr, c_ptr, c_ptr, c_ptr, c_ptr]),
+    "hata_shard_select": (c_i32, [c_ptr, c_ptr, c_i64, c_i32, c_i32, c_i32, c_i32, c_i32, c_i32, c_ptr, c_i64,
+                                  c_i64, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr]),
     "hata_shard_partial_attn": (c_i32, [c_ptr, c_ptr, c_ptr, Strides, c_i32, c_ptr, c_ptr, c_i32, c_i32, c_i32,
-                                        c_i32, c_i32, c_f32, c_ptr, c_ptr]),
+                                        c_i32, c_i32, c_f32, c_i32, c_ptr, c_ptr]),
     "hata_shard_combine": (c_i32, [c_ptr, c_i32, c_i32, c_i32, c_i32, c_ptr, c_i32, c_ptr]),
     "hata_set_option": (c_i32, [c_i32, c_i32]),
     "hata_status_string": (ctypes.c_char_p, [c_i32]),

@@ -226,22 +226,26 @@ hata_status hata_shard_candidates(const void* q, hata_dtype dt, const uint32_t* 
                        cand_D, nullptr, nullptr, n_local_max, stream);
 }
 
-hata_status hata_shard_select(const int32_t* all_D, const int32_t* all_idx, int P, int B, int H_kv, int k, int G,
-                              int rbits, const int64_t* n_total, int64_t lo, int64_t hi, int32_t* own_idx,
-                              int32_t* own_cnt, int32_t* sel_idx, int32_t* sel_score, hata_stream_t stream) {
+hata_status hata_shard_select(const int32_t* all_D, const int32_t* all_idx, int64_t rank_stride, int P, int B,
+                              int H_kv, int k, int G, int rbits, const int64_t* n_total, int64_t lo, int64_t hi,
+                              int32_t* own_idx, int32_t* own_cnt, int32_t* sel_idx, int32_t* sel_score,
+                              hata_stream_t stream) {
   if (!all_D || !all_idx || !n_total || !own_idx || !own_cnt || P < 1 || B < 1 || H_kv < 1 || k < 1 || G < 1 ||
-      rbits % 32 || lo < 0 || hi < lo)
+      rbits % 32 || lo < 0 || hi < lo || rank_stride < 0)
     return HATA_ERR_INVALID_ARG;
+  if (rank_stride == 0) rank_stride = (int64_t)B * H_kv * k;
+  if (rank_stride < (int64_t)B * H_kv * k) return HATA_ERR_INVALID_ARG;
   if ((size_t)(G * rbits + 1 + k + 64) * 4 > 200 * 1024) return HATA_ERR_UNSUPPORTED;
-  hata::SelectParams p = {all_D, all_idx, P, B, H_kv, k, G, rbits, n_total, lo, hi, own_idx, own_cnt, sel_idx, sel_score};
+  hata::SelectParams p = {all_D, all_idx, P, B, H_kv, k, G, rbits, rank_stride, n_total, lo, hi, own_idx, own_cnt,
+                          sel_idx, sel_score};
   return cuda_status(hata::launch_shard_select(p, reinterpret_cast<cudaStream_t>(stream)));
 }
 
 hata_status hata_shard_partial_attn(const void* q, const void* K, const void* V, hata_strides kvs, hata_dtype dt,
                                     const int32_t* own_idx, const int32_t* own_cnt, int B, int H_q, int H_kv, int d,
-                                    int k, float scale, float* partial, hata_stream_t stream) {
+                                    int k, float scale, int splits, float* partial, hata_stream_t stream) {
   if (!q || !K || !V || !own_idx || !own_cnt || !partial || B < 1 || H_kv < 1 || H_q % H_kv || k < 1 ||
-      !dtype_ok(dt))
+      splits < 1 || !dtype_ok(dt))
     return HATA_ERR_INVALID_ARG;
   if (!shape_supported(d, 128, H_q / H_kv)) return HATA_ERR_UNSUPPORTED;
   if (!kv_layout_ok(K, kvs, elem_bytes(dt), d) || !kv_layout_ok(V, kvs, elem_bytes(dt), d)) return HATA_ERR_INVALID_ARG;
@@ -251,6 +255,7 @@ hata_status hata_shard_partial_attn(const void* q, const void* K, const void* V,
   p.B = B; p.Hq = H_q; p.Hkv = H_kv; p.G = H_q / H_kv; p.d = d; p.k = k;
   p.scale = scale != 0.f ? scale : 1.0f / sqrtf((float)d);
   p.partial = partial;
+  p.splits = splits;
   const int G = H_q / H_kv;
   const int GT = hata::group_template(G);
   return cuda_status(hata::launch_partial_attn(p, GT, dt == HATA_BF16, reinterpret_cast<cudaStream_t>(stream)));

@@ -212,4 +212,72 @@ __device__ __forceinline__ void attend_rows_mma(const int32_t* rows, int Rr, con
   HATA_TRACE_AT(tr, 30);
 }
 
+// ---------------------------------------------------------------------------
+// Sequence-shard phase 3 (hata_shard_partial_attn): attention over a split of
+// the rank's selected rows -> raw (m, l, acc) partials.
+template <typename T, int GT, int D_HEAD>
+__global__ void __launch_bounds__(DEC_THREADS, 1) hata_partial_attn_kernel(const __grid_constant__ PartialParams p) {
+  extern __shared__ __align__(1024) uint8_t psm[];
+  constexpr int EB = sizeof(T);
+  constexpr int NSL = AttnState<GT, D_HEAD>::NSL;
+  const int sp = blockIdx.x, u = blockIdx.y, b = u / p.Hkv, g = u % p.Hkv, G = p.G;
+  const int tid = threadIdx.x;
+  const int QS = dec_qstride(D_HEAD);
+  const int rowb = D_HEAD * EB + DEC_ROW_PAD;
+  uint8_t* kv = psm;                                                         // [2][rows_cap][rowb]
+  float* sc = reinterpret_cast<float*>(psm + ((2 * p.rows_cap * rowb + 127) & ~127));   // [GT][rows_cap]
+  float* qf = sc + GT * p.rows_cap;                                          // [GT][QS]
+  float* fm = qf + GT * QS;                                                  // m, l, corr
+  uint64_t* bars = reinterpret_cast<uint64_t*>(fm + 32);                     // 2 mbarriers (bf16 gather)
+  T* qraw = reinterpret_cast<T*>(bars + 2);                                  // [GT][d] bf16 rows
+  int32_t* rows = reinterpret_cast<int32_t*>(qraw + GT * D_HEAD);             // this CTA's rows
+  const T* qg = reinterpret_cast<const T*>(p.q) + ((int64_t)b * p.Hq + (int64_t)g * G) * D_HEAD;
+  for (int i = tid; i < G * D_HEAD; i += DEC_THREADS) {
+    qf[(i / D_HEAD) * QS + i % D_HEAD] = Elem<T>::to_f(qg[i]);
+    qraw[i] = qg[i];
+  }
+  // this split's share of the rank's selected rows (ascending, contiguous)
+  const int cnt = p.own_cnt[u];
+  const int r0 = (int)((int64_t)cnt * sp / p.splits), r1 = (int)((int64_t)cnt * (sp + 1) / p.splits);
+  const int nr = r1 - r0;
+  for (int i = tid; i < nr; i += DEC_THREADS) rows[i] = p.own_idx[(int64_t)u * p.k + r0 + i];
+  if (tid == 0) { mbar_init(&bars[0], 1); mbar_init(&bars[1], 1); fence_mbar_init(); }
+  __syncthreads();
+  const T* Kb = reinterpret_cast<const T*>(p.K) + (int64_t)b * p.kv_sb + (int64_t)g * p.kv_sh;
+  const T* Vb = reinterpret_cast<const T*>(p.V) + (int64_t)b * p.kv_sb + (int64_t)g * p.kv_sh;
+  AttnState<GT, D_HEAD> st;
+  float* m_s = fm;
+  float* l_s = fm + 8;
+  float* corr_s = fm + 16;
+  if constexpr (EB == 2) {
+    // tensor-core gather-attention (the decode kernel's phase 4)
+    attend_rows_mma<GT, D_HEAD>(rows, nr, reinterpret_cast<const __nv_bfloat16*>(Kb),
+                                reinterpret_cast<const __nv_bfloat16*>(Vb), p.kv_st,
+                                reinterpret_cast<const __nv_bfloat16*>(qraw), G, p.scale, kv, p.rows_cap, rowb, m_s,
+                                l_s, st, &bars[0], &bars[1],
+                                reinterpret_cast<const uint8_t*>(p.V) == reinterpret_cast<const uint8_t*>(p.K) + D_HEAD * EB &&
+                                    p.kv_st == 2 * D_HEAD);
+  } else {
+    attend_rows<T, GT, D_HEAD>(rows, nr, Kb, Vb, p.kv_st, qf, G, p.scale, kv, sc, p.rows_cap, rowb, m_s, l_s,
+                               corr_s, st);
+  }
+  const int PS = D_HEAD + 2;
+  float* part = p.partial + (int64_t)sp * p.B * p.Hq * PS;
+#pragma unroll
+  for (int s = 0; s < NSL; ++s) {
+    const int sl = tid + s * DEC_THREADS;
+    const int h = sl / (D_HEAD / 2), e2 = sl % (D_HEAD / 2);
+    if (h < G) {
+      float* pr = part + ((int64_t)b * p.Hq + g * G + h) * PS;
+      pr[2 + 2 * e2] = st.acc[s][0];
+      pr[3 + 2 * e2] = st.acc[s][1];
+    }
+  }
+  if (tid < G) {
+    float* pr = part + ((int64_t)b * p.Hq + g * G + tid) * PS;
+    pr[0] = nr > 0 ? m_s[tid] : -INFINITY;
+    pr[1] = nr > 0 ? l_s[tid] : 0.f;
+  }
+}
+
 }  // namespace hata

@@ -209,6 +209,7 @@ static PartialKernel pick_partial(int GT) {
 cudaError_t launch_partial_attn(PartialParams& p, int GT, int is_bf16, cudaStream_t s) {
   PartialKernel kern = is_bf16 ? pick_partial<__nv_bfloat16>(GT) : pick_partial<float>(GT);
   if (!kern) return cudaErrorNotSupported;
+  if (p.splits < 1) return cudaErrorInvalidValue;
   const int eb = is_bf16 ? 2 : 4;
   const int rowb = p.d * eb + DEC_ROW_PAD;
   const int QS = dec_qstride(p.d);
@@ -216,11 +217,11 @@ cudaError_t launch_partial_attn(PartialParams& p, int GT, int is_bf16, cudaStrea
   if (rc > p.k) rc = p.k;
   p.rows_cap = rc;
   const size_t smem = ((2 * (size_t)rc * rowb + 127) & ~(size_t)127) + (size_t)GT * rc * 4 + (size_t)GT * QS * 4 +
-                      32 * 4 + (size_t)p.k * 4;
+                      32 * 4 + 16 + (size_t)GT * p.d * eb + (size_t)p.k * 4;
   if (smem > (size_t)SMEM_LIMIT) return cudaErrorNotSupported;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  kern<<<p.B * p.Hkv, DEC_THREADS, smem, s>>>(p);
+  kern<<<dim3(p.splits, p.B * p.Hkv), DEC_THREADS, smem, s>>>(p);
   return cudaGetLastError();
 }
 

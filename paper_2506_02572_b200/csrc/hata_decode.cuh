@@ -69,7 +69,7 @@ struct DecodeParams {
   int32_t* ws_hist;        // [units, M, hs] exclusive prefix counts cum_r[0..nbins]   (M > 1)
   uint16_t* ws_D;          // [units, M, chunk] D when it does not fit in smem (!d_smem)
   float* ws_part;          // [units, M, GT, d+2]          (M > 1)
-  unsigned* ws_sync;       // [units, 4]: barrier, done (M > 1), threshold hint, -
+  unsigned* ws_sync;       // [units, 4]: barrier, done (M > 1), threshold hint, hint-use counters
   // sequence-shard phase 1 (hata_shard_candidates): stop after the select and
   // emit (D, global index) candidates instead of attending.
   int cand_mode;
@@ -336,53 +336,9 @@ struct PartialParams {
   const int32_t* own_cnt;  // [B, Hkv]
   int B, Hq, Hkv, G, d, k;
   float scale;
-  float* partial;          // [B, Hq, d+2]
+  float* partial;          // [splits, B, Hq, d+2]
   int rows_cap;            // rows per smem batch
+  int splits;              // CTAs per (b, KV head): CTA s attends to rows [s*cnt/S, (s+1)*cnt/S)
 };
-
-template <typename T, int GT, int D_HEAD>
-__global__ void __launch_bounds__(DEC_THREADS, 1) hata_partial_attn_kernel(const __grid_constant__ PartialParams p) {
-  extern __shared__ __align__(1024) uint8_t psm[];
-  constexpr int EB = sizeof(T);
-  constexpr int NSL = AttnState<GT, D_HEAD>::NSL;
-  const int u = blockIdx.x, b = u / p.Hkv, g = u % p.Hkv, G = p.G;
-  const int tid = threadIdx.x;
-  const int QS = dec_qstride(D_HEAD);
-  const int rowb = D_HEAD * EB + DEC_ROW_PAD;
-  uint8_t* kv = psm;                                                         // [2][rows_cap][rowb]
-  float* sc = reinterpret_cast<float*>(psm + ((2 * p.rows_cap * rowb + 127) & ~127));   // [GT][rows_cap]
-  float* qf = sc + GT * p.rows_cap;                                          // [GT][QS]
-  float* fm = qf + GT * QS;                                                  // m, l, corr
-  int32_t* rows = reinterpret_cast<int32_t*>(fm + 32);                       // [k]
-  const T* qg = reinterpret_cast<const T*>(p.q) + ((int64_t)b * p.Hq + (int64_t)g * G) * D_HEAD;
-  for (int i = tid; i < G * D_HEAD; i += DEC_THREADS) qf[(i / D_HEAD) * QS + i % D_HEAD] = Elem<T>::to_f(qg[i]);
-  const int cnt = p.own_cnt[u];
-  for (int i = tid; i < cnt; i += DEC_THREADS) rows[i] = p.own_idx[(int64_t)u * p.k + i];
-  __syncthreads();
-  const T* Kb = reinterpret_cast<const T*>(p.K) + (int64_t)b * p.kv_sb + (int64_t)g * p.kv_sh;
-  const T* Vb = reinterpret_cast<const T*>(p.V) + (int64_t)b * p.kv_sb + (int64_t)g * p.kv_sh;
-  AttnState<GT, D_HEAD> st;
-  float* m_s = fm;
-  float* l_s = fm + 8;
-  float* corr_s = fm + 16;
-  attend_rows<T, GT, D_HEAD>(rows, cnt, Kb, Vb, p.kv_st, qf, G, p.scale, kv, sc, p.rows_cap, rowb, m_s, l_s, corr_s,
-                             st);
-  const int PS = D_HEAD + 2;
-#pragma unroll
-  for (int s = 0; s < NSL; ++s) {
-    const int sl = tid + s * DEC_THREADS;
-    const int h = sl / (D_HEAD / 2), e2 = sl % (D_HEAD / 2);
-    if (h < G) {
-      float* pr = p.partial + ((int64_t)b * p.Hq + g * G + h) * PS;
-      pr[2 + 2 * e2] = st.acc[s][0];
-      pr[3 + 2 * e2] = st.acc[s][1];
-    }
-  }
-  if (tid < G) {
-    float* pr = p.partial + ((int64_t)b * p.Hq + g * G + tid) * PS;
-    pr[0] = m_s[tid];
-    pr[1] = l_s[tid];
-  }
-}
 
 }  // namespace hata

@@ -673,6 +673,13 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
   // [t*WPT, (t+1)*WPT) (token order), visits only the marked tokens, and the
   // picks are emitted in token order from one block scan of the counts
   const bool fast = Th >= 0 && thr >= 0 && thr <= Th;
+  if (p.ws_sync && r == 0 && tid == 0) {
+    // diagnostics word: launches whose selection took the
+    // hinted path (low 16 bits) and whose threshold came from the window
+    // exchange (high 16 bits), per unit, wrapping
+    unsigned* cnt = p.ws_sync + 4 * u + 3;
+    *cnt += (fast ? 1u : 0u) + ((M > 1 && misc[5]) ? 0x10000u : 0u);
+  }
   if (fast) {
     const int WPT = (nbw + DEC_THREADS - 1) / DEC_THREADS;
     // WPTC: compile-time bound on the words per thread (1 for chunks of up

@@ -54,9 +54,10 @@ int group_template(int G);
 cudaError_t launch_decode(DecodeParams& p, const DecodePlan& plan, void* ws, int is_bf16, cudaStream_t s);
 
 struct SelectParams {
-  const int32_t* all_D;    // [P, B, Hkv, k]
-  const int32_t* all_idx;  // [P, B, Hkv, k]
+  const int32_t* all_D;    // [P] blocks of [B, Hkv, k], rank_stride elements apart
+  const int32_t* all_idx;  // same
   int P, B, Hkv, k, G, rbits;
+  int64_t rank_stride;     // elements between consecutive ranks' blocks
   const int64_t* n_total;  // [B]
   int64_t lo, hi;
   int32_t* own_idx;        // [B, Hkv, k]
@@ -68,7 +69,7 @@ cudaError_t launch_shard_select(const SelectParams& p, cudaStream_t s);
 cudaError_t launch_shard_combine(const float* part, int P, int B, int Hq, int d, void* out, int out_bf16,
                                  cudaStream_t s);
 struct PartialParams;
-cudaError_t launch_partial_attn(PartialParams& p, int GT, int is_bf16, cudaStream_t s);
+cudaError_t launch_partial_attn(PartialParams& p, int GT, int is_bf16, cudaStream_t s);   // grid: splits x units
 
 int device_sm_count();
 

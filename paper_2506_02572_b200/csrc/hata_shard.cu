@@ -29,7 +29,7 @@ __global__ void __launch_bounds__(256) shard_select_kernel(SelectParams p) {
   const int E = p.P * p.k;                 // candidate entries
   auto entry = [&](int e, int& D, int& idx) {
     const int rr = e / p.k, i = e % p.k;
-    const int64_t off = (((int64_t)rr * p.B * p.Hkv) + bg) * p.k + i;
+    const int64_t off = (int64_t)rr * p.rank_stride + (int64_t)bg * p.k + i;
     idx = p.all_idx[off];
     D = idx >= 0 ? p.all_D[off] : 0x7fffffff;
   };

@@ -7,16 +7,22 @@ are replicated.  One decode step (Alg. 3, split over token ranges):
   0. append   the rank holding row n[b]-1 writes k_new/v_new and its key code
               (Alg. 3 lines 2-9) -- hata_append, rows of other ranks skipped;
   1. local    q-hash + Hamming score + local top-k' candidates (D, global idx)
-              (Alg. 3 lines 6, 10-13 on the slice) -- hata_shard_candidates;
-  C1          all-gather of the candidates (NCCL; 8 B x k per (b, g) per rank);
+              (Alg. 3 lines 6, 10-13 on the slice) -- hata_shard_candidates,
+              written into ONE packed [2, B, H_kv, k] int32 buffer (D | idx);
+  C1          one all-gather of the packed candidates (NCCL; 8 B x k per (b, g)
+              per rank);
   2. select   global k' smallest (D, idx) -- identical on every rank, and equal
               to the unsharded selection: any global top-k' token is in its
               shard's local top-k', and because ranges ascend with the rank,
               "lowest index wins" (R8) is "lower rank first, then local order"
               -- hata_shard_select;
-  3. partial  attention over the own selected rows -> (m, l, acc) -- hata_shard_partial_attn;
-  C2          all-gather of the partials (fp32, (d+2) x H_q per b per rank);
-  4. combine  rank-ordered flash-decoding merge -- hata_shard_combine.
+  3. partial  attention over the own selected rows, split over S CTAs per
+              (b, g) on the tensor cores -> S x (m, l, acc) -- hata_shard_partial_attn;
+  C2          all-gather of the partials (fp32, S x (d+2) x H_q per b per rank);
+  4. combine  rank- then split-ordered flash-decoding merge -- hata_shard_combine.
+
+Every step is stream-ordered with no host synchronisation, so a whole step
+(kernels and NCCL collectives) can be captured in one CUDA graph.
 
 The collectives are the only host-visible exchange; every arithmetic step is
 one of libhata's kernels.  ``ops`` defaults to the CUDA library; it exists so
@@ -37,8 +43,10 @@ def shard_range(cap_total: int, world: int, rank: int):
 
 
 def _all_gather(t: torch.Tensor, world: int, group=None) -> torch.Tensor:
-    """Rank-major stack [P, ...] of ``t`` from every rank."""
-    if world == 1:
+    """Rank-major stack [P, ...] of ``t`` from every rank (NCCL: one
+    all_gather_into_tensor, also at world size 1 when a process group exists)."""
+    if not dist.is_initialized():
+        assert world == 1
         return t.unsqueeze(0)
     if dist.get_backend(group) == "nccl":
         out = torch.empty((world,) + tuple(t.shape), dtype=t.dtype, device=t.device)
@@ -57,7 +65,7 @@ class SeqShardDecode:
     """
 
     def __init__(self, K, V, codes, W, Hq: int, k: int, cap_total: int, rank: int, world: int, group=None,
-                 ops=None, out_dtype=torch.float32):
+                 ops=None, out_dtype=torch.float32, splits: int | None = None):
         if ops is None:
             import paper_2506_02572_b200 as ops
         self.ops = ops
@@ -71,13 +79,17 @@ class SeqShardDecode:
         assert self.hi - self.lo <= self.C, "local slice smaller than the owned range"
         dev = K.device
         B, Hkv = self.B, self.Hkv
-        self.cand_D = torch.empty(B, Hkv, k, dtype=torch.int32, device=dev)
-        self.cand_idx = torch.empty(B, Hkv, k, dtype=torch.int32, device=dev)
+        self.cand = torch.empty(2, B, Hkv, k, dtype=torch.int32, device=dev)   # packed (D | idx): one collective
+        self.cand_D, self.cand_idx = self.cand[0], self.cand[1]
         self.own_idx = torch.empty(B, Hkv, k, dtype=torch.int32, device=dev)
         self.own_cnt = torch.empty(B, Hkv, dtype=torch.int32, device=dev)
         self.sel_idx = torch.empty(B, Hkv, k, dtype=torch.int32, device=dev)
         self.sel_score = torch.empty(B, Hkv, k, dtype=torch.int32, device=dev)
-        self.partial = torch.empty(B, Hq, self.d + 2, dtype=torch.float32, device=dev)
+        if splits is None:   # CTAs per (b, KV head) for the partial attention: fill the SMs once
+            sms = torch.cuda.get_device_properties(dev).multi_processor_count if K.is_cuda else 1
+            splits = max(1, min(16, sms // max(1, B * Hkv)))
+        self.splits = splits
+        self.partial = torch.empty(splits, B, Hq, self.d + 2, dtype=torch.float32, device=dev)
         self.out = torch.empty(B, Hq, self.d, dtype=out_dtype, device=dev)
         self.workspace = None
         if hasattr(ops, "decode_workspace_size") and K.is_cuda:
@@ -116,14 +128,14 @@ class SeqShardDecode:
         return self.partial
 
     def phase_combine(self, parts):
-        """Step 4: rank-ordered combine of the gathered partials."""
-        self.ops.shard_combine(parts, self.out)
+        """Step 4: rank-ordered (then split-ordered) combine of the gathered
+        partials [P, S, B, H_q, d+2]."""
+        self.ops.shard_combine(parts.reshape(-1, *parts.shape[-3:]), self.out)
         return self.out
 
     def step(self, q, n, n_max: int, k_new=None, v_new=None, scale: float = 0.0):
         """One decode step; returns out [B, H_q, d] (identical on every rank)."""
-        cand_D, cand_idx = self.phase_local(q, n, n_max, k_new, v_new)
-        all_D = _all_gather(cand_D, self.world, self.group)
-        all_idx = _all_gather(cand_idx, self.world, self.group)
-        part = self.phase_select_attend(q, n, all_D, all_idx, scale)
+        self.phase_local(q, n, n_max, k_new, v_new)
+        allc = _all_gather(self.cand, self.world, self.group)          # [P, 2, B, H_kv, k]
+        part = self.phase_select_attend(q, n, allc[:, 0], allc[:, 1], scale)
         return self.phase_combine(_all_gather(part, self.world, self.group))

@@ -125,3 +125,59 @@ def test_shard_parity_cfg4(P):
     st = check_decode(case, g, shape.k, code_rows_sample=65536)
     assert e <= 2e-3
     print(P, st, e)
+
+
+def _nccl_worker(port, q):
+    import os
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK="0", WORLD_SIZE="1")
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", 0))
+    try:
+        import paper_2506_02572_b200 as H
+        from paper_2506_02572_b200.seqshard import SeqShardDecode
+        shape = _shape("cfg2", N=8192, k=256)
+        case = synth.make_case(shape, seed=23, device="cuda")
+        K, V, W = case["K"].contiguous(), case["V"].contiguous(), case["W"].contiguous()
+        codes = torch.zeros(1, shape.Hkv, shape.N, 4, dtype=torch.int32, device="cuda")
+        H.hash_keys(K, W, codes, 0, shape.N - 1)
+        Kf, Vf, cf = K.clone(), V.clone(), codes.clone()
+        n = case["n_before"] + 1
+        ref_idx = torch.full((1, shape.Hkv, shape.k), -7, dtype=torch.int32, device="cuda")
+        ref = H.decode_step(case["q"], case["k_new"], case["v_new"], Kf, Vf, cf, W, n, shape.k, out_idx=ref_idx)
+        rk = SeqShardDecode(K, V, codes, W, shape.Hq, shape.k, shape.N, 0, 1)
+        # the collective path (NCCL all_gather_into_tensor), eager and captured in a CUDA graph
+        out = rk.step(case["q"], n, shape.N, case["k_new"], case["v_new"]).clone()
+        g = torch.cuda.CUDAGraph()
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            rk.step(case["q"], n, shape.N, case["k_new"], case["v_new"])
+        torch.cuda.current_stream().wait_stream(s)
+        with torch.cuda.graph(g):
+            gout = rk.step(case["q"], n, shape.N, case["k_new"], case["v_new"])
+        g.replay()
+        torch.cuda.synchronize()
+        q.put((bool(torch.equal(rk.sel_idx, ref_idx)), float((out - ref).abs().max()), float((gout - ref).abs().max())))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_seqshard_nccl_collective_path():
+    """The NCCL branch of the exchange (all_gather_into_tensor of the packed
+    candidates and of the partials), at world size 1 on one GPU, eagerly and
+    inside a CUDA graph: equal to the unsharded fused step."""
+    import socket
+    import torch.multiprocessing as mp
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = ctx.Process(target=_nccl_worker, args=(port, q))
+    p.start()
+    same_idx, e_eager, e_graph = q.get(timeout=300)
+    p.join(timeout=60)
+    assert p.exitcode == 0
+    assert same_idx
+    assert e_eager <= 2e-3 and e_graph <= 2e-3, (e_eager, e_graph)

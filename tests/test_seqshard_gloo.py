@@ -79,23 +79,27 @@ class CpuOps:
 
     @staticmethod
     def shard_partial_attn(q, K, V, own_idx, own_cnt, k, partial, scale=0.0):
+        # partial [S, B, H_q, d+2]: split s takes rows [s*cnt/S, (s+1)*cnt/S) (as the kernel does)
+        S = partial.shape[0]
         B, Hq, d = q.shape
         G = Hq // K.shape[1]
         sc = scale or 1.0 / np.sqrt(d)
-        for b in range(B):
-            for h in range(Hq):
-                g = h // G
-                rows = own_idx[b, g, :int(own_cnt[b, g])].long()
-                if len(rows) == 0:
-                    partial[b, h, 0] = -float("inf")
-                    partial[b, h, 1:] = 0
-                    continue
-                z = (K[b, g, rows].double() @ q[b, h].double()) * sc
-                m = z.max()
-                e = torch.exp(z - m)
-                partial[b, h, 0] = m
-                partial[b, h, 1] = e.sum()
-                partial[b, h, 2:] = e @ V[b, g, rows].double()
+        for s in range(S):
+            for b in range(B):
+                for h in range(Hq):
+                    g = h // G
+                    cnt = int(own_cnt[b, g])
+                    rows = own_idx[b, g, cnt * s // S:cnt * (s + 1) // S].long()
+                    if len(rows) == 0:
+                        partial[s, b, h, 0] = -float("inf")
+                        partial[s, b, h, 1:] = 0
+                        continue
+                    z = (K[b, g, rows].double() @ q[b, h].double()) * sc
+                    m = z.max()
+                    e = torch.exp(z - m)
+                    partial[s, b, h, 0] = m
+                    partial[s, b, h, 1] = e.sum()
+                    partial[s, b, h, 2:] = e @ V[b, g, rows].double()
 
     @staticmethod
     def shard_combine(parts, out):
@@ -139,7 +143,7 @@ def _worker(rank, world, port, shape_kw, seed, nb, resq):
         for b in range(shape.B):
             codes_full[b, :, int(nb[b]):] = 0
         rk = SeqShardDecode(sl(K), sl(V), sl(codes_full), W, shape.Hq, shape.k, cap, rank, world, ops=CpuOps,
-                            out_dtype=torch.float64)
+                            out_dtype=torch.float64, splits=2)
         n = case["n_before"] + 1
         out = rk.step(case["q"].double(), n, int(n.max()), case["k_new"].double(), case["v_new"].double())
         resq.put((rank, out.numpy().copy(), rk.sel_idx.numpy().copy()))
