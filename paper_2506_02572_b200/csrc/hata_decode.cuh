@@ -31,7 +31,7 @@ constexpr int DEC_D_SMEM_MAX = 16384;        // tokens/CTA whose D (u16) stays i
 constexpr int DEC_CHUNK_ALIGN = 64;          // tokens
 constexpr int DEC_BC_WPT = 4;               // candidate-bitmap words per thread (fast selection path)
 constexpr int DEC_HINT_SLACK = 2;           // hint threshold slack (bins)
-constexpr int DEC_WIN = 8;                  // bins [Th - 6, Th + 1] of every rank's prefix counts read with the totals
+constexpr int DEC_WIN = 32;                 // bins [h - 15, h + 16] (h = previous threshold) of every rank's prefix counts
 constexpr int DEC_MAX_RANKS = 32;            // M cap (histogram exchange is M x nbins per rank)
 constexpr int DEC_ROW_PAD = 16;              // bytes of padding per staged K/V row (bank spread)
 constexpr int DEC_QS_PAD = 4;                // floats of padding per q row in smem
@@ -159,7 +159,7 @@ __host__ __device__ inline DecodeSmem decode_smem_layout(const DecodeParams& p, 
   s.planes = off; off += up((64 + 8) * 4);        // P/N planes [2][4][8] + K0 shares [8]
   s.rows = off; off += p.ws_rows ? 0 : up(p.R_cap * 4);
   s.red = off; off += up((DEC_MAX_RANKS * 4 + 64) * 4);
-  s.chref = off; off += up(DEC_MAX_RANKS * 32);
+  s.chref = off; off += up(DEC_MAX_RANKS * DEC_WIN * 4);
   s.misc = off; off += up(128 * 4);   // [0,16) scalars, [16,80) warp counters, [80,104) softmax m/l/corr
   s.qp = off; off += up(DEC_THREADS * (GT + 1) * 4);
   s.total = off;

@@ -215,7 +215,10 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
   const int NV = G + (owner ? 1 : 0);                                // projected vectors
   mbar_wait(&bars[NST], 0);                                         // W_g in smem
   __syncthreads();                                                  // q, k_new, v_new, hint in smem
-  if (hinted) { const int h = misc[14]; Th = h > 0 ? h + DEC_HINT_SLACK : -1; }
+  // previous threshold h: the candidate bitmap marks D <= Th = h + slack; the
+  // exchange reads every rank's prefix counts at the window [hw0, hw0 + DEC_WIN)
+  int hw0 = 0;
+  if (hinted) { const int h = misc[14]; Th = h > 0 ? h + DEC_HINT_SLACK : -1; hw0 = h - (DEC_WIN / 2 - 1); }
   HATA_TRACE(9);
   if constexpr (EB != 2) {                                          // fp32 paths read q as floats
     for (int i = tid; i < NV * D_HEAD; i += DEC_THREADS) qf[(i / D_HEAD) * QS + i % D_HEAD] = Elem<T>::to_f(qraw[i]);
@@ -549,15 +552,17 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
     // [w0, w0 + DEC_WIN) around it: the unit totals there give the threshold
     // when it falls in the window, and the per-rank values the tie quota --
     // one round trip, no unit-total atomics
-    const int w0 = Th - (DEC_WIN - 2);
-    if (Th >= 0 && tid < M * DEC_WIN) {
-      const int rr = tid / DEC_WIN, bi = w0 + tid % DEC_WIN;
-      win[tid] = (bi >= 0 && bi <= p.nbins) ? __ldcg(gu + (int64_t)rr * hs + bi) : 0;
-    }
+    const int w0 = hw0;
+    if (Th >= 0)
+      for (int i = tid; i < M * DEC_WIN; i += DEC_THREADS) {
+        const int rr = i / DEC_WIN, bi = w0 + i % DEC_WIN;
+        win[i] = (bi >= 0 && bi <= p.nbins) ? __ldcg(gu + (int64_t)rr * hs + bi) : 0;
+      }
     __syncthreads();
+    static_assert(DEC_WIN == 32, "one lane per window bin");
     if (warp == 0) {
       int tot = 0;
-      if (Th >= 0 && lane < DEC_WIN)
+      if (Th >= 0)
         for (int rr = 0; rr < M; ++rr) tot += win[rr * DEC_WIN + lane];
       const int z = __shfl_down_sync(0xffffffffu, tot, 1);
       const int bj = w0 + lane;                                       // bins bj, bj + 1 both in the window
@@ -569,20 +574,21 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
     __syncthreads();
     if (!misc[5] && kp > 0) {
       // no hint, or the threshold is outside the window: unit totals of
-      // every bin from the M ranks' published prefix counts
-      int acc[BPT_MAX + 1];
+      // every bin from the M ranks' published prefix counts -- thread per
+      // bin, all M loads in flight (one round trip), totals in the code
+      // ring (free after scoring), then the crossing bin
+      int32_t* tots = reinterpret_cast<int32_t*>(ring);
+      for (int j = tid; j <= p.nbins; j += DEC_THREADS) {
+        int t8[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 #pragma unroll
-      for (int q = 0; q <= BPT_MAX; ++q) acc[q] = 0;
-      for (int rr = 0; rr < M; ++rr) {
-        const int32_t* cr = gu + (int64_t)rr * hs;
-#pragma unroll
-        for (int q = 0; q <= BPT_MAX; ++q)
-          if (q <= BPT && i0 + q <= p.nbins) acc[q] += __ldcg(cr + i0 + q);
+        for (int rr = 0; rr < DEC_MAX_RANKS; ++rr)
+          if (rr < M) t8[rr & 7] += __ldcg(gu + (int64_t)rr * hs + j);
+        tots[j] = ((t8[0] + t8[1]) + (t8[2] + t8[3])) + ((t8[4] + t8[5]) + (t8[6] + t8[7]));
       }
-#pragma unroll
-      for (int q = 0; q < BPT_MAX; ++q) {
-        const int i = i0 + q;
-        if (q < BPT && i < p.nbins && acc[q] < kp && kp <= acc[q + 1]) { misc[0] = i; misc[1] = kp - acc[q]; }
+      __syncthreads();
+      for (int j = tid; j < p.nbins; j += DEC_THREADS) {
+        const int a = tots[j], z = tots[j + 1];
+        if (a < kp && kp <= z) { misc[0] = j; misc[1] = kp - a; }
       }
     }
   } else {
@@ -605,7 +611,7 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
   int quota = need, off0 = 0;
   int bl = 0, ti = 0;
   if (M > 1 && thr >= 0 && lane < M) {
-    const int w0 = Th - (DEC_WIN - 2);                                // window bins [w0, w0 + DEC_WIN)
+    const int w0 = hw0;                                               // window bins [w0, w0 + DEC_WIN)
     if (Th >= 0 && thr >= w0 && thr + 1 < w0 + DEC_WIN) {
       bl = win[lane * DEC_WIN + thr - w0];
       ti = win[lane * DEC_WIN + thr + 1 - w0];
