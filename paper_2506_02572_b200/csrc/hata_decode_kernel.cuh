@@ -92,6 +92,8 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
   if (HATA_DIAG && (p.dbg & 4)) return;                            // diagnostics: launch cost only
 
   const int M = p.M;
+  const bool d_smem = p.d_smem;
+  const int cand_mode = p.cand_mode;
   const int NST = p.stages;
   const int r = blockIdx.x;
   const int u = blockIdx.y;
@@ -106,7 +108,7 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.bars);  // [NST] ring, [NST] W, [NST+1] exchange, [NST+2] partials
   uint32_t* hist = reinterpret_cast<uint32_t*>(smem + L.hist);
   uint16_t* Dglob = p.ws_D ? p.ws_D + ((int64_t)u * M + r) * dec_dchunk(p.chunk) : nullptr;
-  uint16_t* Dloc = p.d_smem ? reinterpret_cast<uint16_t*>(smem + L.D) : Dglob;
+  uint16_t* Dloc = d_smem ? reinterpret_cast<uint16_t*>(smem + L.D) : Dglob;
   uint16_t* Ds = reinterpret_cast<uint16_t*>(smem + L.D);          // Dloc when d_smem (shared-space stores)
   float* qf = reinterpret_cast<float*>(smem + L.qf);
   uint32_t* qw = reinterpret_cast<uint32_t*>(smem + L.qw);
@@ -195,7 +197,7 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
   // selection visits only the marked tokens; otherwise it scans all of D.
   // A hint changes the work done, never the result.
   uint32_t* Bc = reinterpret_cast<uint32_t*>(smem + L.bc);
-  const int nbw = p.d_smem ? dec_dchunk(p.chunk) / 32 : 0;          // bitmap words
+  const int nbw = d_smem ? dec_dchunk(p.chunk) / 32 : 0;          // bitmap words
   int Th = -1;
   const bool hinted = p.use_hint && p.ws_sync && nbw > 0 && nbw <= DEC_BC_WPT * DEC_THREADS;
   const int kp = (int)(n < (int64_t)p.k ? n : (int64_t)p.k);      // k' = min(k, n)  (R10)
@@ -368,53 +370,40 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
       for (int w = 0; w < W; ++w) kc[w] = st[j * W + w];
     }
   };
-  int slot = 0;
-  uint32_t parity = 0;
-  for (int s = 0; s < nstages; ++s) {
-    if (!(HATA_DIAG && (p.dbg & 16))) mbar_wait(&bars[slot], parity);   // dbg 16: timing without waiting for the stream
-    if (s == 0) HATA_TRACE(10);
-    if (s == nstages - 1) HATA_TRACE(13);
-    const int base = s * STAGE_TOK;
-    const int nval = min(STAGE_TOK, Lr - base);                     // valid tokens (< n), may be <= 0
-    const int copied = (int)(((uint32_t)(min(STAGE_TOK, Lcopy - base) * W * 4) & ~15u) / (W * 4));
-    const int npairs = max(0, min(nval, copied)) / 2;
-    const uint32_t* st = reinterpret_cast<const uint32_t*>(ring + slot * DEC_STAGE_BYTES);
-    uint32_t* dst = reinterpret_cast<uint32_t*>(Dloc + base);
-    uint32_t* dsts = reinterpret_cast<uint32_t*>(Ds + base);        // same, as a shared-space pointer
-    // two token pairs per thread per iteration (independent chains for ILP);
-    // a pair -> one 32-bit store of two u16 distances.  (One pair per
-    // iteration is faster in isolation -- probes/probe_score2.cu -- but
-    // measured 0.8 us slower per step in this kernel.)
-    for (int j2 = tid; j2 < npairs; j2 += 2 * DEC_THREADS) {
-      const int j2b = j2 + DEC_THREADS;
-      const bool two = j2b < npairs;
-      uint32_t k0[W], k1[W], k2[W], k3[W];
-      smem_code(st, 2 * j2, k0);
-      smem_code(st, 2 * j2 + 1, k1);
-      if (two) {
-        smem_code(st, 2 * j2b, k2);
-        smem_code(st, 2 * j2b + 1, k3);
+  // one token pair -> one 32-bit store of two u16 distances; SCORE_PAIRS
+  // pairs per thread per iteration (independent chains for ILP)
+  auto score_pairs = [&](const uint32_t* st, uint32_t* dst, uint32_t* dsts, int npairs) {
+#ifndef HATA_SCORE_PAIRS
+#define HATA_SCORE_PAIRS 1                                          // measured: 1 beats 2 by ~0.1 us/step (flat loop)
+#endif
+    constexpr int SP = HATA_SCORE_PAIRS;
+    for (int j2 = tid; j2 < npairs; j2 += SP * DEC_THREADS) {
+      uint32_t kc[SP][2][W];
+      bool ok[SP];
+#pragma unroll
+      for (int q = 0; q < SP; ++q) {
+        const int jq = j2 + q * DEC_THREADS;
+        ok[q] = q == 0 || jq < npairs;
+        if (ok[q]) { smem_code(st, 2 * jq, kc[q][0]); smem_code(st, 2 * jq + 1, kc[q][1]); }
       }
-      const uint32_t d0 = group_D(k0);
-      const uint32_t d1 = group_D(k1);
-      const uint32_t d2 = group_D(k2);
-      const uint32_t d3 = group_D(k3);
-      if (!(HATA_DIAG && (p.dbg & 2))) {                            // dbg 2: timing without the histogram
-        atomicAdd(&hist[d0], 1u);
-        atomicAdd(&hist[d1], 1u);
-      }
-      if (p.d_smem) dsts[j2] = d0 | (d1 << 16);
-      else dst[j2] = d0 | (d1 << 16);
-      if (two) {
-        if (!(HATA_DIAG && (p.dbg & 2))) {
-          atomicAdd(&hist[d2], 1u);
-          atomicAdd(&hist[d3], 1u);
+      uint32_t d[SP][2];
+#pragma unroll
+      for (int q = 0; q < SP; ++q) { d[q][0] = group_D(kc[q][0]); d[q][1] = group_D(kc[q][1]); }
+#pragma unroll
+      for (int q = 0; q < SP; ++q) {
+        if (!ok[q]) continue;
+        if (!(HATA_DIAG && (p.dbg & 2))) {                            // dbg 2: timing without the histogram
+          atomicAdd(&hist[d[q][0]], 1u);
+          atomicAdd(&hist[d[q][1]], 1u);
         }
-        if (p.d_smem) dsts[j2b] = d2 | (d3 << 16);
-        else dst[j2b] = d2 | (d3 << 16);
+        const int jq = j2 + q * DEC_THREADS;
+        if (d_smem) dsts[jq] = d[q][0] | (d[q][1] << 16);
+        else dst[jq] = d[q][0] | (d[q][1] << 16);
       }
     }
-    // leftovers: an odd last token, or tokens past the 16-byte-rounded copy
+  };
+  // leftovers: an odd last token, or tokens past the 16-byte-rounded copy
+  auto score_rest = [&](const uint32_t* st, int base, int nval, int copied, int npairs) {
     const int rest = nval - 2 * npairs;
     if (tid < rest) {
       const int j = 2 * npairs + tid;
@@ -430,11 +419,40 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
       atomicAdd(&hist[dv], 1u);
       Dloc[base + j] = (uint16_t)dv;
     }
-    if (recycle) {                                                  // refill the slot just consumed
-      __syncthreads();
+  };
+  auto copied_tok = [&](int s) {                                   // tokens of stage s fully in smem
+    return (int)(((uint32_t)(min(STAGE_TOK, Lcopy - s * STAGE_TOK) * W * 4) & ~15u) / (W * 4));
+  };
+  if (!recycle) {
+    // the whole chunk fits the ring (and was streamed before the wait): one
+    // flat pass over it once every stage has landed
+    for (int s = 0; s < nstages; ++s)
+      if (!(HATA_DIAG && (p.dbg & 16))) mbar_wait(&bars[s], 0u);
+    HATA_TRACE(10);
+    const int copied = nstages ? (nstages - 1) * STAGE_TOK + copied_tok(nstages - 1) : 0;
+    const int npairs = max(0, min(Lr, copied)) / 2;
+    score_pairs(reinterpret_cast<const uint32_t*>(ring), reinterpret_cast<uint32_t*>(Dloc),
+                reinterpret_cast<uint32_t*>(Ds), npairs);
+    score_rest(reinterpret_cast<const uint32_t*>(ring), 0, Lr, copied, npairs);
+    HATA_TRACE(13);
+  } else {
+    int slot = 0;
+    uint32_t parity = 0;
+    for (int s = 0; s < nstages; ++s) {
+      if (!(HATA_DIAG && (p.dbg & 16))) mbar_wait(&bars[slot], parity);   // dbg 16: timing without waiting for the stream
+      if (s == 0) HATA_TRACE(10);
+      if (s == nstages - 1) HATA_TRACE(13);
+      const int base = s * STAGE_TOK;
+      const int nval = min(STAGE_TOK, Lr - base);                     // valid tokens (< n), may be <= 0
+      const int copied = copied_tok(s);
+      const int npairs = max(0, min(nval, copied)) / 2;
+      const uint32_t* st = reinterpret_cast<const uint32_t*>(ring + slot * DEC_STAGE_BYTES);
+      score_pairs(st, reinterpret_cast<uint32_t*>(Dloc + base), reinterpret_cast<uint32_t*>(Ds + base), npairs);
+      score_rest(st, base, nval, copied, npairs);
+      __syncthreads();                                              // the slot is consumed: refill it
       if (tid == 0 && s + NST < nstages) issue_stage(s + NST);
+      if (++slot == NST) { slot = 0; parity ^= 1u; }
     }
-    if (++slot == NST) { slot = 0; parity ^= 1u; }
   }
   __syncthreads();                                                  // every D / histogram update done
   if (owner && tid == 0) {
@@ -830,7 +848,7 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
   float* l_s = fmisc + 88;
   float* corr_s = fmisc + 96;
   AttnState<GT, D_HEAD> st;
-  if (!p.cand_mode) {
+  if (!cand_mode) {
     const T* Kb = reinterpret_cast<const T*>(p.K) + (int64_t)b * p.kv_sb + (int64_t)g * p.kv_sh;
     const T* Vb = reinterpret_cast<const T*>(p.V) + (int64_t)b * p.kv_sb + (int64_t)g * p.kv_sh;
     if constexpr (EB == 2) {
@@ -866,7 +884,7 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
     else reinterpret_cast<float*>(p.out)[oi] = v;
   };
   if (M == 1) {
-    if (!p.cand_mode) {
+    if (!cand_mode) {
 #pragma unroll
       for (int s = 0; s < NSL; ++s) {
         const int sl = tid + s * DEC_THREADS;
@@ -884,7 +902,7 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
   const int PS = D_HEAD + 2;
   const int PB = dec_part_stride(GT, D_HEAD);
   float* mypart = p.ws_part + ((int64_t)u * M + r) * PB;
-  if (!p.cand_mode) {
+  if (!cand_mode) {
 #pragma unroll
     for (int s = 0; s < NSL; ++s) {
       const int sl = tid + s * DEC_THREADS;
@@ -911,7 +929,7 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
   HATA_TRACE(15);
   // rank 0: every partial is visible (writer release + counter); merge them
   // in rank order straight from L2 (thread = one output element)
-  if (!p.cand_mode) {
+  if (!cand_mode) {
     // merge weights once per head: warp h (< G) holds rank r in lane r,
     // w[r][h] = e^{m_r - M_h} and 1 / L_h go to smem; every output thread
     // issues its M partial loads up front (one L2 round trip)
