@@ -8,7 +8,12 @@
  *
  * CONVENTIONS (all entry points)
  *  - Every pointer is caller-owned DEVICE memory unless stated otherwise; the
- *    library never allocates, frees or synchronises.  Work is enqueued on
+ *    library never allocates, frees or synchronises.  HATA-off (P:421-422,
+ *    KV offloading): the K and V caches of hata_append / hata_decode_topk_attn
+ *    / hata_decode_step may instead be page-locked HOST memory mapped into the
+ *    device address space (cudaHostAlloc under UVA); the code cache stays in
+ *    device memory, so only the selected K/V rows cross the host link, fetched
+ *    by the decode kernel's own gather.  Work is enqueued on
  *    `stream` (a cudaStream_t; NULL = legacy default stream) and is
  *    asynchronous: outputs are valid once the stream reaches that point.
  *  - Argument validation is synchronous and happens before any launch; on a

@@ -64,6 +64,15 @@ def _need_cuda(*ts):
             raise HataError("all tensors must be CUDA tensors (no CPU path)")
 
 
+def _need_kv(K, V):
+    """K/V caches: CUDA tensors, or -- HATA-off -- pinned host
+    tensors, which CUDA maps into the device address space (UVA): the decode
+    kernel gathers only the selected rows from host memory itself."""
+    for t in (K, V):
+        if not (t.is_cuda or (t.device.type == "cpu" and t.is_pinned())):
+            raise HataError("K/V must be CUDA tensors or pinned host tensors (HATA-off)")
+
+
 def set_option(name: str, value: int):
     """hata_set_option: "selection_hint", "pdl" or "cooperative" (process-wide, default on)."""
     opt = {"selection_hint": _lib.HATA_OPT_SELECTION_HINT, "pdl": _lib.HATA_OPT_PDL,
@@ -85,7 +94,8 @@ def hash_keys(K, W, codes, t0: int = 0, n: int | None = None, stream=None):
 
 def append(k_new, v_new, W, K, V, codes, pos, stream=None):
     """Alg. 3 lines 2-9: write k_new/v_new and HashEncode(k_new) at row pos[b] (in place)."""
-    _need_cuda(k_new, v_new, W, K, V, codes, pos)
+    _need_cuda(k_new, v_new, W, codes, pos)
+    _need_kv(K, V)
     k_new, v_new = k_new.contiguous(), v_new.contiguous()
     B, Hkv, cap, d = K.shape
     if K.stride() != V.stride():
@@ -108,7 +118,8 @@ def decode_topk_attn(q, K, V, codes, W, n, k: int, n_max: int | None = None, sca
                      stream=None):
     """Alg. 3 lines 6, 10-17 over caches already holding the new token.
     Returns ``out`` [B, H_q, d]."""
-    _need_cuda(q, K, V, codes, W, n)
+    _need_cuda(q, codes, W, n)
+    _need_kv(K, V)
     q = q.contiguous()
     B, Hq, d = q.shape
     Hkv, rbits = K.shape[1], W.shape[2]
@@ -133,7 +144,8 @@ def decode_step(q, k_new, v_new, K, V, codes, W, n, k: int, n_max: int | None = 
                 stream=None):
     """Alg. 3 lines 2-17 in one launch: append k_new/v_new (and the key code) at
     row n[b]-1, then decode.  ``n`` counts the new token.  Returns ``out``."""
-    _need_cuda(q, k_new, v_new, K, V, codes, W, n)
+    _need_cuda(q, k_new, v_new, codes, W, n)
+    _need_kv(K, V)
     q, k_new, v_new = q.contiguous(), k_new.contiguous(), v_new.contiguous()
     B, Hq, d = q.shape
     Hkv, cap, rbits = K.shape[1], K.shape[2], W.shape[2]
