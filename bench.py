@@ -385,6 +385,56 @@ def bench_offload(sh, steps, device):
                     "selected rows from mapped host memory; the appended row is written there by the same launch"}
 
 
+class PagedStep:
+    """A Step whose caches are moved into physical page pools ([pages, H_kv,
+    ps, 2, d] K/V, [pages, H_kv, ps, W] codes) in a random page order,
+    addressed through a block table (NEXT-2)."""
+
+    def __init__(self, st, ps, seed):
+        sh = st.sh
+        B, Hkv, cap, d = st.K.shape
+        self.st, self.ps = st, ps
+        maxp = -(-cap // ps)
+        npages = B * maxp
+        g = torch.Generator().manual_seed(seed)
+        perm = torch.randperm(npages, generator=g).view(B, maxp)
+        dev = st.K.device
+        kv = torch.zeros(npages, Hkv, ps, 2, d, dtype=st.K.dtype, device=dev)
+        self.codes = torch.zeros(npages, Hkv, ps, sh.rbits // 32, dtype=torch.int32, device=dev)
+        for b in range(B):
+            for lp in range(maxp):
+                a, z = lp * ps, min(cap, (lp + 1) * ps)
+                pp = int(perm[b, lp])
+                kv[pp, :, :z - a, 0] = st.K[b, :, a:z]
+                kv[pp, :, :z - a, 1] = st.V[b, :, a:z]
+                self.codes[pp, :, :z - a] = st.codes[b, :, a:z]
+        self.K, self.V = kv[:, :, :, 0], kv[:, :, :, 1]
+        self.pt = perm.to(torch.int32).to(dev)
+        st.K = st.V = st.codes = None
+
+    def run(self, r=0):
+        st = self.st
+        st.H.decode_step_paged(st.qs[r], st.kn, st.vn, self.K, self.V, self.codes, st.W, self.pt, st.n, st.sh.k,
+                               n_max=st.sh.N, out=st.out, workspace=st.ws)
+
+
+def bench_paged(sh, ps, steps, device, peak, n_sets=N_SETS):
+    """NEXT-2: the CFG-4 step over paged pools (page size ps, pages shuffled),
+    same rotation / graph / query variation as the contiguous bench line."""
+    sets = [PagedStep(Step(sh, 1000 + i, device), ps, 77 + i) for i in range(n_sets)]
+    torch.cuda.empty_cache()
+    graphs = [_graph(lambda r=r: [st.run(r) for st in sets]) for r in range(N_Q)]
+    for g in graphs:
+        g.replay()
+    reps = max(1, steps // n_sets)
+    t, per = time_replays([(graphs[i % N_Q], n_sets) for i in range(reps)])
+    us = t / (reps * n_sets) * 1e6
+    b = algorithmic_bytes(sh)
+    return {"workload": f"{sh.name} over paged pools (page size {ps}, pages in random order)", "us_per_step": us,
+            "tokens_per_s": tokens_per_s(sh.B, us), "unit": UNIT, "frac": b / (us * 1e-6) / 1e9 / peak,
+            "p5_us": _pct(per, 5), "p95_us": _pct(per, 95)}
+
+
 def secondary_line(sh, steps, warmup, device, peak):
     r = bench_single(sh, steps, warmup, device, clocks=False)
     us = r["t_step"] / r["steps"] * 1e6
@@ -733,6 +783,8 @@ def main_single(args, sh, device, peak, peak_src, opts):
         sec["cfg5_32_layers"] = dict({"workload": "cfg5: Qwen2.5-14B-shaped full 32-layer decode step, 1 GPU",
                                       "unit": UNIT}, **m)
         sec["hata_off_cfg2"] = bench_offload(synth.CONFIGS["cfg2"], 64, device)
+        sec["paged_cfg4_ps64"] = bench_paged(synth.CONFIGS["cfg4"], 64, 208, device, peak)
+        torch.cuda.empty_cache()
         line["secondary"] = sec
     st = Step(sh, 1000, device, n_q=1)
     line["hash_keys"] = bench_hash_keys(st, 20)

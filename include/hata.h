@@ -182,6 +182,34 @@ hata_status hata_decode_step(const void* q, const void* k_new, const void* v_new
                              void* out, hata_dtype out_dt, int32_t* out_idx, int32_t* out_score,
                              uint32_t* out_qcodes, void* workspace, size_t ws_bytes, hata_stream_t stream);
 
+/* ------------------------------------------------------------------------
+ * hata_decode_step_paged -- hata_decode_step over PAGED caches (the block
+ * tables of serving engines; "pluggable into ... FlashInfer/vLLM").
+ * Logical token t of sequence b lives in slot t % page_size of physical page
+ * page_table[b * max_pages + t / page_size].
+ *   K, V   physical pools, element strides kvs = {page stride, head stride,
+ *          token stride}, d contiguous (e.g. [pages, H_kv, page_size, 2, d]
+ *          with V = K + d: one bulk copy per selected token).
+ *   codes  physical pool [pages, H_kv, page_size, rbits/32], word strides
+ *          cs = {page stride, head stride, rbits/32}; page and head strides
+ *          multiples of 4 words.
+ *   page_table  DEVICE int32 [B, max_pages]; entries for pages holding
+ *          tokens < n[b] must be valid (the page of row n[b]-1 included: the
+ *          step appends there).  The code stream of a paged launch starts
+ *          after griddepcontrol.wait (the table may be written by the
+ *          preceding kernel).
+ *   page_size  a power of two with page_size * rbits/8 a multiple of 16.
+ * bf16 only (UNSUPPORTED otherwise); n_max > max_pages * page_size ->
+ * CAPACITY; everything else as hata_decode_step.  The prefill hash of a pool
+ * is hata_hash_keys over the pool viewed as [pages, H_kv, page_size, d].
+ * ------------------------------------------------------------------------ */
+hata_status hata_decode_step_paged(const void* q, const void* k_new, const void* v_new, void* K, void* V,
+                                   hata_strides kvs, hata_dtype dt, uint32_t* codes, hata_strides cs,
+                                   const int32_t* page_table, int max_pages, int page_size, const void* W, int B,
+                                   int H_q, int H_kv, int d, int rbits, const int64_t* n, int64_t n_max, int k,
+                                   float scale, void* out, hata_dtype out_dt, int32_t* out_idx, int32_t* out_score,
+                                   uint32_t* out_qcodes, void* workspace, size_t ws_bytes, hata_stream_t stream);
+
 /* Bytes of device workspace hata_decode_topk_attn needs for this shape
  * (0 when everything fits on chip).  Host-only; never fails (0 on bad args). */
 size_t hata_decode_workspace_size(int B, int H_q, int H_kv, int d, int rbits, int64_t n_max, int k,

@@ -18,7 +18,7 @@ import torch
 from . import _lib
 from ._lib import HataError, Strides  # noqa: F401
 
-__all__ = ["set_option", "hash_keys", "append", "decode_topk_attn", "decode_step", "decode_workspace_size", "decode_ranks",
+__all__ = ["set_option", "hash_keys", "append", "decode_topk_attn", "decode_step", "decode_step_paged", "decode_workspace_size", "decode_ranks",
            "shard_candidates", "shard_select", "shard_partial_attn", "shard_combine", "HataError", "lib"]
 
 
@@ -163,6 +163,34 @@ def decode_step(q, k_new, v_new, K, V, codes, W, n, k: int, n_max: int | None = 
         _p(codes), _strides4(codes), _p(W), B, Hq, Hkv, d, rbits, _p(n), n_max, cap, k, scale, _p(out), _dt(out),
         _p(out_idx), _p(out_score), _p(out_qcodes), _p(workspace) if ws else None, ws, _stream(stream)),
         "hata_decode_step")
+    return out
+
+
+def decode_step_paged(q, k_new, v_new, K, V, codes, W, page_table, n, k: int, n_max: int, scale: float = 0.0,
+                      out=None, out_dtype=torch.float32, out_idx=None, out_score=None, out_qcodes=None,
+                      workspace=None, stream=None):
+    """hata_decode_step over paged pools.  K, V: [pages, H_kv, page_size, d]
+    views (any page/head/token strides, d contiguous); codes: [pages, H_kv,
+    page_size, rbits//32]; page_table: int32 [B, max_pages] on the device."""
+    _need_cuda(q, k_new, v_new, codes, W, page_table, n)
+    _need_kv(K, V)
+    q, k_new, v_new = q.contiguous(), k_new.contiguous(), v_new.contiguous()
+    B, Hq, d = q.shape
+    Hkv, page_size, rbits = K.shape[1], K.shape[2], W.shape[2]
+    if page_table.dtype != torch.int32 or page_table.dim() != 2 or not page_table.is_contiguous():
+        raise HataError("page_table must be a contiguous int32 [B, max_pages] tensor")
+    if out is None:
+        out = torch.empty(B, Hq, d, dtype=out_dtype, device=q.device)
+    if K.stride() != V.stride():
+        raise HataError("K and V must share strides")
+    ws = decode_workspace_size(B, Hq, Hkv, d, rbits, n_max, k, K.dtype)
+    if ws and (workspace is None or workspace.numel() * workspace.element_size() < ws):
+        workspace = torch.zeros(ws, dtype=torch.uint8, device=q.device)
+    _lib.check(lib().hata_decode_step_paged(
+        _p(q), _p(k_new), _p(v_new), _p(K), _p(V), _strides4(K), _dt(K), _p(codes), _strides4(codes),
+        _p(page_table), page_table.shape[1], page_size, _p(W), B, Hq, Hkv, d, rbits, _p(n), n_max, k, scale,
+        _p(out), _dt(out), _p(out_idx), _p(out_score), _p(out_qcodes), _p(workspace) if ws else None, ws,
+        _stream(stream)), "hata_decode_step_paged")
     return out
 
 

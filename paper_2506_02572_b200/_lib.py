@@ -42,6 +42,9 @@ _SIGS = {
     "hata_decode_step": (c_i32, [c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, Strides, c_i32, c_ptr, Strides, c_ptr, c_i32,
                                  c_i32, c_i32, c_i32, c_i32, c_ptr, c_i64, c_i64, c_i32, c_f32, c_ptr, c_i32, c_ptr,
                                  c_ptr, c_ptr, c_ptr, c_size, c_ptr]),
+    "hata_decode_step_paged": (c_i32, [c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, Strides, c_i32, c_ptr, Strides, c_ptr,
+                                       c_i32, c_i32, c_ptr, c_i32, c_i32, c_i32, c_i32, c_i32, c_ptr, c_i64, c_i32,
+                                       c_f32, c_ptr, c_i32, c_ptr, c_ptr, c_ptr, c_ptr, c_size, c_ptr]),
     "hata_decode_workspace_size": (c_size, [c_i32, c_i32, c_i32, c_i32, c_i32, c_i64, c_i32, c_i32]),
     "hata_decode_ranks": (c_i32, [c_i32, c_i32, c_i32, c_i32, c_i32, c_i64, c_i32, c_i32]),
     "hata_shard_candidates": (c_i32, [c_ptr, c_i32, c_ptr, Strides, c_ptr, c_i32, c_i32, c_i32, c_i32, c_i32, c_ptr,

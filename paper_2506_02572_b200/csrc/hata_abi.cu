@@ -167,7 +167,8 @@ static hata_status decode_common(const void* q, const void* K, const void* V, ha
                                  hata_dtype out_dt, int32_t* out_idx, int32_t* out_score, uint32_t* out_qcodes,
                                  void* workspace, size_t ws_bytes, int cand_mode, int64_t token_offset,
                                  int32_t* cand_D, const void* k_new, const void* v_new, int64_t cap,
-                                 hata_stream_t stream) {
+                                 hata_stream_t stream, const int32_t* page_table = nullptr, int max_pages = 0,
+                                 int page_lg = 0) {
   if (!q || !codes || !W || !n || B < 1 || H_kv < 1 || H_q < H_kv || H_q % H_kv || rbits < 32 || rbits % 32 ||
       n_max < 0 || k < 1 || !dtype_ok(dt))
     return HATA_ERR_INVALID_ARG;
@@ -190,6 +191,7 @@ static hata_status decode_common(const void* q, const void* K, const void* V, ha
   p.out_idx = out_idx; p.out_score = out_score; p.out_qcodes = out_qcodes;
   p.cand_mode = cand_mode; p.token_offset = token_offset; p.cand_D = cand_D;
   p.k_new = k_new; p.v_new = v_new; p.cap = cap;
+  p.page_table = page_table; p.max_pages = max_pages; p.page_lg = page_lg;
   return cuda_status(hata::launch_decode(p, pl, workspace, dt == HATA_BF16, reinterpret_cast<cudaStream_t>(stream)));
 }
 
@@ -212,6 +214,26 @@ hata_status hata_decode_step(const void* q, const void* k_new, const void* v_new
   if (!aligned(k_new, 16) || !aligned(v_new, 16)) return HATA_ERR_INVALID_ARG;
   return decode_common(q, K, V, kvs, dt, codes, cs, W, B, H_q, H_kv, d, rbits, n, n_max, k, scale, out, out_dt,
                        out_idx, out_score, out_qcodes, workspace, ws_bytes, 0, 0, nullptr, k_new, v_new, cap, stream);
+}
+
+hata_status hata_decode_step_paged(const void* q, const void* k_new, const void* v_new, void* K, void* V,
+                                   hata_strides kvs, hata_dtype dt, uint32_t* codes, hata_strides cs,
+                                   const int32_t* page_table, int max_pages, int page_size, const void* W, int B,
+                                   int H_q, int H_kv, int d, int rbits, const int64_t* n, int64_t n_max, int k,
+                                   float scale, void* out, hata_dtype out_dt, int32_t* out_idx, int32_t* out_score,
+                                   uint32_t* out_qcodes, void* workspace, size_t ws_bytes, hata_stream_t stream) {
+  if (!k_new || !v_new || !page_table || max_pages < 1 || page_size < 1) return HATA_ERR_INVALID_ARG;
+  int lg = 0;
+  while ((1 << lg) < page_size) ++lg;
+  if ((1 << lg) != page_size) return HATA_ERR_INVALID_ARG;                  // a power of two
+  if (dt != HATA_BF16) return HATA_ERR_UNSUPPORTED;
+  if (((int64_t)page_size * (rbits / 32) * 4) % 16 || cs.sb % 4 || cs.sh % 4) return HATA_ERR_INVALID_ARG;
+  if (n_max > (int64_t)max_pages * page_size) return HATA_ERR_CAPACITY;
+  if (!aligned(k_new, 16) || !aligned(v_new, 16)) return HATA_ERR_INVALID_ARG;
+  // kvs / cs: {page stride, head stride, token stride}; a sequence's capacity is max_pages pages
+  return decode_common(q, K, V, kvs, dt, codes, cs, W, B, H_q, H_kv, d, rbits, n, n_max, k, scale, out, out_dt,
+                       out_idx, out_score, out_qcodes, workspace, ws_bytes, 0, 0, nullptr, k_new, v_new,
+                       (int64_t)max_pages * page_size, stream, page_table, max_pages, lg);
 }
 
 hata_status hata_shard_candidates(const void* q, hata_dtype dt, const uint32_t* codes, hata_strides cs,

@@ -16,8 +16,8 @@
 namespace hata {
 
 template <int GT, int D_HEAD>
-__device__ __forceinline__ void attend_rows_mma(const int32_t* rows, int Rr, const __nv_bfloat16* __restrict__ Kb,
-                                                const __nv_bfloat16* __restrict__ Vb, int64_t kv_st, const __nv_bfloat16* qb,
+__device__ __forceinline__ void attend_rows_mma(const int32_t* rows, int Rr, const __nv_bfloat16* __restrict__ Kc,
+                                                const __nv_bfloat16* __restrict__ Vc, RowMap rmap, const __nv_bfloat16* qb,
                                                 int G, float scale, uint8_t* kvbuf, int rows_cap, int rowb,
                                                 float* m_s, float* l_s, AttnState<GT, D_HEAD>& st,
                                                 uint64_t* bar, uint64_t* bar2, int kvpair, unsigned long long* tr = nullptr,
@@ -69,11 +69,11 @@ __device__ __forceinline__ void attend_rows_mma(const int32_t* rows, int Rr, con
     // bulk copies one lane after another, so spread them over all warps
     if (kvpair) {
       for (int i = lane * DEC_WARPS + warp; i < nb; i += DEC_THREADS)
-        bulk_g2s(Kj + i * rowb, Kb + (int64_t)rows[r0 + i] * kv_st, 2 * ROWBYTES, (j ? bar2 : bar));
+        bulk_g2s(Kj + i * rowb, Kc + rmap(rows[r0 + i]), 2 * ROWBYTES, (j ? bar2 : bar));
     } else {
       for (int i = lane * DEC_WARPS + warp; i < 2 * nb; i += DEC_THREADS) {
         const int which = i >= nb, rr = i - (which ? nb : 0);
-        const __nv_bfloat16* src = (which ? Vb : Kb) + (int64_t)rows[r0 + rr] * kv_st;
+        const __nv_bfloat16* src = (which ? Vc : Kc) + rmap(rows[r0 + rr]);
         bulk_g2s((which ? Vj : Kj) + rr * rowb, src, ROWBYTES, (j ? bar2 : bar));
       }
     }
@@ -251,8 +251,9 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_partial_attn_kernel(const
   float* corr_s = fm + 16;
   if constexpr (EB == 2) {
     // tensor-core gather-attention (the decode kernel's phase 4)
-    attend_rows_mma<GT, D_HEAD>(rows, nr, reinterpret_cast<const __nv_bfloat16*>(Kb),
-                                reinterpret_cast<const __nv_bfloat16*>(Vb), p.kv_st,
+    attend_rows_mma<GT, D_HEAD>(rows, nr, reinterpret_cast<const __nv_bfloat16*>(p.K),
+                                reinterpret_cast<const __nv_bfloat16*>(p.V),
+                                RowMap{nullptr, 0, 0, (int64_t)b * p.kv_sb + (int64_t)g * p.kv_sh, p.kv_st},
                                 reinterpret_cast<const __nv_bfloat16*>(qraw), G, p.scale, kv, p.rows_cap, rowb, m_s,
                                 l_s, st, &bars[0], &bars[1],
                                 reinterpret_cast<const uint8_t*>(p.V) == reinterpret_cast<const uint8_t*>(p.K) + D_HEAD * EB &&

@@ -40,6 +40,20 @@ constexpr int DEC_QS_PAD = 4;                // floats of padding per q row in s
 #define HATA_SPIN_LIMIT (1u << 24)
 #endif
 
+// Element (or word) offset of token t's row for one (b, KV head): contiguous
+// caches (pt == null): base + t * st with base = b * sb + g * sh; paged caches
+// (NEXT-2, P:260 serving engines): page table row pt of sequence b, rows of a
+// physical page ps = 2^lg apart: pt[t >> lg] * sp + base + (t & (ps-1)) * st
+// with base = g * sh.
+struct RowMap {
+  const int32_t* pt;
+  int lg;
+  int64_t sp, base, st;
+  __device__ __forceinline__ int64_t operator()(int64_t t) const {
+    return pt ? (int64_t)__ldg(pt + (t >> lg)) * sp + base + (t & ((1 << lg) - 1)) * st : base + t * st;
+  }
+};
+
 struct DecodeParams {
   const void* q;           // [B, Hq, d] contiguous
   const void* K;           // caches, element strides, d contiguous
@@ -81,6 +95,11 @@ struct DecodeParams {
   // n[b]-1 before scoring; null = caches already hold the new token
   const void* k_new;       // [B, Hkv, d]
   const void* v_new;
+  // paged caches (hata_decode_step_paged): logical token t of sequence b is
+  // slot t & (2^page_lg - 1) of physical page page_table[b * max_pages +
+  // (t >> page_lg)]; kv_sb / c_sb are then the page strides.  null = contiguous
+  const int32_t* page_table;
+  int max_pages, page_lg;
   unsigned long long* trace;   // diagnostics (hata_debug_trace), null = off
   int dbg;                     // diagnostics: HATA_DEBUG bits (0 in production)
   int use_hint;                // threshold hint from the previous launch (HATA_HINT=0 disables)

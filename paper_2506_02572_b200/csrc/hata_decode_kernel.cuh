@@ -126,7 +126,12 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
   const int Lcopy = (int)max((int64_t)0, min((int64_t)per, p.n_max - t0));   // rows streamed
   const int nstages = (Lcopy + STAGE_TOK - 1) / STAGE_TOK;
   const bool recycle = nstages > NST;                              // ring smaller than the chunk
-  const uint32_t* cbase = p.codes + (int64_t)b * p.c_sb + (int64_t)g * p.c_sh;
+  // row maps of this unit's code cache (words) and K/V caches (elements)
+  const int32_t* ptab = p.page_table ? p.page_table + (int64_t)b * p.max_pages : nullptr;
+  const RowMap cmap{ptab, p.page_lg, p.c_sb, ptab ? (int64_t)g * p.c_sh : (int64_t)b * p.c_sb + (int64_t)g * p.c_sh,
+                    (int64_t)W};
+  const RowMap kvmap{ptab, p.page_lg, p.kv_sb,
+                     ptab ? (int64_t)g * p.kv_sh : (int64_t)b * p.kv_sb + (int64_t)g * p.kv_sh, p.kv_st};
   const T* qg = reinterpret_cast<const T*>(p.q) + ((int64_t)b * p.Hq + (int64_t)g * G) * D_HEAD;
   const bool append = p.k_new != nullptr;
   T* qraw = reinterpret_cast<T*>(smem + L.qraw);                    // [G (+1 key)][d] as stored
@@ -140,12 +145,30 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
   // launch appends itself is rescored from its own k_new.  q, k_new, v_new,
   // n and the workspace are read after the wait with plain loads (not queued
   // behind the stream's TMA requests).
+  // stage s of the code chunk into ring slot s % NST; called by a whole warp
+  // (contiguous caches: lane 0 issues one copy; paged: lane i copies the
+  // i-th page segment of the stage, the segments' bytes summing to the
+  // stage's -- every segment but the chunk's last is a multiple of 16 bytes)
   auto issue_stage = [&](int s) {
     const int slot = s % NST;
     const int ntok = min(STAGE_TOK, Lcopy - s * STAGE_TOK);
     const uint32_t bytes = (uint32_t)(ntok * W * 4) & ~15u;
-    mbar_arrive_expect_tx(&bars[slot], bytes);
-    if (bytes) bulk_g2s(ring + slot * DEC_STAGE_BYTES, cbase + (t0 + (int64_t)s * STAGE_TOK) * W, bytes, &bars[slot]);
+    const int64_t ts = t0 + (int64_t)s * STAGE_TOK;
+    if (lane == 0) mbar_arrive_expect_tx(&bars[slot], bytes);
+    __syncwarp();
+    if (!ptab) {
+      if (lane == 0 && bytes) bulk_g2s(ring + slot * DEC_STAGE_BYTES, p.codes + cmap(ts), bytes, &bars[slot]);
+    } else {
+      const int ps = 1 << p.page_lg;
+      const int64_t first = ts >> p.page_lg, last = (ts + ntok - 1) >> p.page_lg;
+      for (int64_t pg = first + lane; ntok > 0 && pg <= last; pg += 32) {
+        const int64_t a = max(ts, pg << p.page_lg), z = min(ts + (int64_t)ntok, (pg + 1) << p.page_lg);
+        const uint32_t off = (uint32_t)((a - ts) * W * 4);
+        const uint32_t nb = min((uint32_t)((z - a) * W * 4), bytes > off ? bytes - off : 0u) & ~15u;
+        if (nb) bulk_g2s(ring + slot * DEC_STAGE_BYTES + off, p.codes + cmap(a), nb, &bars[slot]);
+      }
+      (void)ps;
+    }
   };
   const int WROWB = dec_wrow_stride(p.rbits, EB);                   // padded smem row of W_g
   const uint32_t wrow = (uint32_t)(p.rbits * EB);                  // bytes of one W_g row
@@ -165,7 +188,7 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
       bulk_g2s(reinterpret_cast<uint8_t*>(Ws) + row * WROWB, wsrc + (int64_t)row * p.rbits, wrow, &bars[NST]);
   }
   __syncthreads();                                                  // W_g requests ahead of the stream
-  if (tid == 0)                                                     // the code chunk, a few large copies
+  if (warp == 0 && !ptab)                                           // the code chunk, a few large copies
     for (int s = 0; s < NST && s < nstages; ++s) issue_stage(s);
   for (int i = tid; i < p.nbins; i += DEC_THREADS) hist[i] = 0;
   // Programmatic dependent launch: everything above reads only the hash
@@ -190,6 +213,8 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
       dq[i] = __ldcg(reinterpret_cast<const uint4*>(src) + c);
     }
     if (tid == 0) misc[14] = p.ws_sync ? (int)__ldcg(p.ws_sync + 4 * u + 2) : 0;
+    if (warp == 0 && ptab)                                          // paged: the page table is read after the wait
+      for (int s = 0; s < NST && s < nstages; ++s) issue_stage(s);
   }
   // Candidate hint: the unit's threshold of the previous launch on this
   // workspace (+ DEC_HINT_SLACK).  Tokens with D <= Th are marked in a bitmap
@@ -321,7 +346,7 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
     const int h = i / W, w = i % W;
     const uint32_t word = qw[i];
     if (h < G && p.out_qcodes && r == 0) p.out_qcodes[((int64_t)b * p.Hq + g * G + h) * W + w] = word;
-    if (h == G) const_cast<uint32_t*>(p.codes)[(int64_t)b * p.c_sb + (int64_t)g * p.c_sh + pos * W + w] = word;
+    if (h == G) const_cast<uint32_t*>(p.codes)[cmap(pos) + w] = word;
   }
   // signed-weight planes of w_b = G - 2 c_b, c_b = #{h: q_h bit b set}
   // (hata_score.cuh): P_j / N_j and the constant K0, one warp per code word
@@ -411,7 +436,7 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
       if (j < copied) {
         smem_code(st, j, kc);
       } else {
-        const uint32_t* gp = cbase + (t0 + base + j) * W;
+        const uint32_t* gp = p.codes + cmap(t0 + base + j);
 #pragma unroll
         for (int w = 0; w < W; ++w) kc[w] = __ldg(gp + w);
       }
@@ -450,7 +475,7 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
       score_pairs(st, reinterpret_cast<uint32_t*>(Dloc + base), reinterpret_cast<uint32_t*>(Ds + base), npairs);
       score_rest(st, base, nval, copied, npairs);
       __syncthreads();                                              // the slot is consumed: refill it
-      if (tid == 0 && s + NST < nstages) issue_stage(s + NST);
+      if (warp == 0 && s + NST < nstages) issue_stage(s + NST);
       if (++slot == NST) { slot = 0; parity ^= 1u; }
     }
   }
@@ -472,8 +497,7 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
     // this rank's arrival at the exchange so that every rank's gather sees them
     constexpr int CH = D_HEAD * EB / 16;
     if (tid < 2 * CH) {
-      T* dstrow = const_cast<T*>(reinterpret_cast<const T*>(tid < CH ? p.K : p.V)) + (int64_t)b * p.kv_sb +
-                  (int64_t)g * p.kv_sh + pos * p.kv_st;
+      T* dstrow = const_cast<T*>(reinterpret_cast<const T*>(tid < CH ? p.K : p.V)) + kvmap(pos);
       const uint4 v = reinterpret_cast<const uint4*>(qraw + (tid < CH ? G : G + 1) * D_HEAD)[tid % CH];
       reinterpret_cast<uint4*>(dstrow)[tid % CH] = v;
       asm volatile("fence.proxy.async.global;" ::: "memory");        // this rank's own gather reads it by TMA
@@ -852,7 +876,9 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
     const T* Kb = reinterpret_cast<const T*>(p.K) + (int64_t)b * p.kv_sb + (int64_t)g * p.kv_sh;
     const T* Vb = reinterpret_cast<const T*>(p.V) + (int64_t)b * p.kv_sb + (int64_t)g * p.kv_sh;
     if constexpr (EB == 2) {
-      attend_rows_mma<GT, D_HEAD>(rows, Rr, Kb, Vb, p.kv_st, reinterpret_cast<const __nv_bfloat16*>(qraw), G, p.scale, smem + L.kv, p.rows_cap, L.rb,
+      attend_rows_mma<GT, D_HEAD>(rows, Rr, reinterpret_cast<const __nv_bfloat16*>(p.K),
+                                  reinterpret_cast<const __nv_bfloat16*>(p.V), kvmap,
+                                  reinterpret_cast<const __nv_bfloat16*>(qraw), G, p.scale, smem + L.kv, p.rows_cap, L.rb,
                                   m_s, l_s, st, &bars[NST + 3], &bars[NST + 2],
                                   reinterpret_cast<const uint8_t*>(p.V) == reinterpret_cast<const uint8_t*>(p.K) + D_HEAD * EB &&
                                       p.kv_st == 2 * D_HEAD,
