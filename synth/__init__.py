@@ -127,3 +127,27 @@ def random_codes(n_rows: int, rbits: int, seed: int, pool: int | None = None):
     base = torch.randint(0, 2**32, (pool, W), generator=g, dtype=torch.int64)
     pick = torch.randint(0, pool, (n_rows,), generator=g)
     return base[pick]
+
+
+def make_training_sequence(n: int, d: int, G: int, seed: int, device="cpu", topics: int = 16,
+                           offset: float = 3.0):
+    """Synthetic prefill activations of one KV head for hash training (NEXT-3):
+    anisotropic keys and queries with a large shared offset (a common key bias
+    direction, as in LLM keys) and topic structure (position t belongs to topic
+    c(t); its key and its G queries share the topic direction), so exact
+    top-k attention is structured and sign(x W) with random W wastes bits on
+    the shared offset.  Returns Q [n, G, d], K [n, d] (fp32).  No method
+    arithmetic: draws only."""
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+
+    def randn(*sz):
+        return torch.randn(*sz, generator=g, device=device, dtype=torch.float32)
+    scale = 0.2 + 2.0 * torch.exp(-torch.arange(d, device=device, dtype=torch.float32) / (d / 4))
+    mu_k = offset * randn(d)
+    mu_q = offset * randn(d)
+    topic = 2.0 * randn(topics, d)
+    c = torch.randint(0, topics, (n,), generator=g, device=device)
+    K = mu_k + scale * (randn(n, d) + topic[c])
+    Q = mu_q + scale * (randn(n, G, d) + topic[c][:, None, :])
+    return Q, K
