@@ -332,6 +332,45 @@ def bench_hash_keys(st, reps):
             "note": f"K ({kbytes / 1e6:.0f} MB) exceeds the 126 MB L2; {reps} back-to-back calls"}
 
 
+def bench_prefill_write(st, reps):
+    """NEXT-1: a whole prefilled chunk (B*H_kv*(N-1) keys and values) written
+    into the paired cache with its codes in one pass (hata_prefill_write) vs
+    the separate copy + hata_hash_keys."""
+    sh = st.sh
+    n = sh.N - 1
+    B, Hkv, cap, d = st.K.shape
+    g = torch.Generator(device=st.K.device).manual_seed(5)
+    Ks = torch.randn(B, Hkv, n, d, generator=g, device=st.K.device).to(st.K.dtype)
+    Vs = torch.randn_like(Ks)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+
+    def fused():
+        st.H.prefill_write(Ks, Vs, st.W, st.K, st.V, st.codes, 0)
+
+    def separate():
+        st.K[:, :, :n].copy_(Ks)
+        st.V[:, :, :n].copy_(Vs)
+        st.H.hash_keys(st.K, st.W, st.codes, 0, n)
+    fused(); separate()
+    torch.cuda.synchronize()
+    ev[0].record()
+    for _ in range(reps):
+        fused()
+    ev[1].record()
+    for _ in range(reps):
+        separate()
+    ev[2].record()
+    ev[2].synchronize()
+    uf = ev[0].elapsed_time(ev[1]) / reps * 1e3
+    us = ev[1].elapsed_time(ev[2]) / reps * 1e3
+    eb = 2 if sh.dtype == "bf16" else 4
+    io = 4 * B * Hkv * n * d * eb + B * Hkv * n * sh.rbits // 8      # read K, V + write K, V + codes
+    peak, _ = _peaks()
+    return {"us": uf, "separate_copy_plus_hash_keys_us": us, "algorithmic_bytes": io,
+            "GBps": io / (uf * 1e-6) / 1e9, "frac_of_hbm": io / (uf * 1e-6) / 1e9 / peak,
+            "kernel": "hash_keys_umma_kernel<FUSED> (TMA loads of the chunk, TMA stores to the cache, tcgen05 hash)"}
+
+
 def dense_baseline(st, steps):
     """Full-attention decode over the same cache (context, north_star)."""
     q = st.q.view(st.sh.B, st.sh.Hq, 1, st.sh.d)
@@ -788,6 +827,7 @@ def main_single(args, sh, device, peak, peak_src, opts):
         line["secondary"] = sec
     st = Step(sh, 1000, device, n_q=1)
     line["hash_keys"] = bench_hash_keys(st, 20)
+    line["prefill_write"] = bench_prefill_write(st, 10)
     line["dense_baseline"] = dense_baseline(st, 50)
     line["dense_baseline"]["speedup_vs_dense"] = line["dense_baseline"]["us_per_step"] / us
     del st

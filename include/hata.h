@@ -90,6 +90,27 @@ hata_status hata_hash_keys(const void* K, hata_strides ks, hata_dtype dt, const 
                            hata_stream_t stream);
 
 /* ------------------------------------------------------------------------
+ * hata_prefill_write -- write a prefilled chunk into the caches AND hash its
+ * keys in one pass (Alg. 1 lines 2-5; the codes
+ * come from the K tiles already on chip, so hashing costs no extra HBM read
+ * of K -- P:250-251).
+ *   K_src, V_src [B, H_kv, n, d] chunk (strides ss; d contiguous).
+ *   K, V         caches (strides kvs): rows [t0, t0 + n) of every (b, g) are
+ *                written; no other row is touched.
+ *   codes        rows [t0, t0 + n) = HashEncode(K_src rows) (strides cs).
+ * Both sides must be covered by 3-D tensor maps: batch stride = H_kv x head
+ * stride, 16-byte aligned rows.  bf16 only; tcgen05 tensor cores (the
+ * hata_hash_keys kernel with a store warp that writes the staged K and V
+ * tiles to the caches by TMA).
+ * Errors: INVALID_ARG, CAPACITY (t0 + n > cap), UNSUPPORTED (dtype, d, rbits,
+ *         strides no 3-D tensor map covers), CUDA.
+ * ------------------------------------------------------------------------ */
+hata_status hata_prefill_write(const void* K_src, const void* V_src, hata_strides ss, void* K, void* V,
+                               hata_strides kvs, hata_dtype dt, const void* W, int B, int H_kv, int d, int rbits,
+                               int64_t t0, int64_t n, int64_t cap, uint32_t* codes, hata_strides cs,
+                               hata_stream_t stream);
+
+/* ------------------------------------------------------------------------
  * hata_append -- decode-time cache update for the new token.
  * PAPER: Alg. 3 "HATA Decode Stage" lines 2-9: K^cache <- [K^cache; K],
  * V^cache <- [V^cache; V], K_H <- HashEncode(K), K_H^cache <- [K_H^cache; K_H];

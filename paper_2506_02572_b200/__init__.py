@@ -18,7 +18,7 @@ import torch
 from . import _lib
 from ._lib import HataError, Strides  # noqa: F401
 
-__all__ = ["set_option", "hash_keys", "append", "decode_topk_attn", "decode_step", "decode_step_paged", "decode_workspace_size", "decode_ranks",
+__all__ = ["set_option", "hash_keys", "prefill_write", "append", "decode_topk_attn", "decode_step", "decode_step_paged", "decode_workspace_size", "decode_ranks",
            "shard_candidates", "shard_select", "shard_partial_attn", "shard_combine", "HataError", "lib"]
 
 
@@ -90,6 +90,19 @@ def hash_keys(K, W, codes, t0: int = 0, n: int | None = None, stream=None):
     _lib.check(lib().hata_hash_keys(_p(K), _strides4(K), _dt(K), _p(W), B, Hkv, d, rbits, t0, n, cap,
                                     _p(codes), _strides4(codes), _stream(stream)), "hata_hash_keys")
     return codes
+
+
+def prefill_write(K_src, V_src, W, K, V, codes, t0: int = 0, stream=None):
+    """NEXT-1: K/V chunk [B, H_kv, n, d] -> cache rows [t0, t0+n) and their
+    codes, keys read once (hata_prefill_write)."""
+    _need_cuda(K_src, V_src, W, K, V, codes)
+    W = W.contiguous()
+    B, Hkv, n, d = K_src.shape
+    if K_src.stride() != V_src.stride() or K.stride() != V.stride():
+        raise HataError("K and V must share strides (source and cache)")
+    _lib.check(lib().hata_prefill_write(_p(K_src), _p(V_src), _strides4(K_src), _p(K), _p(V), _strides4(K), _dt(K),
+                                        _p(W), B, Hkv, d, W.shape[2], t0, n, K.shape[2], _p(codes), _strides4(codes),
+                                        _stream(stream)), "hata_prefill_write")
 
 
 def append(k_new, v_new, W, K, V, codes, pos, stream=None):

@@ -34,6 +34,8 @@ class Strides(ctypes.Structure):
 _SIGS = {
     "hata_hash_keys": (c_i32, [c_ptr, Strides, c_i32, c_ptr, c_i32, c_i32, c_i32, c_i32, c_i64, c_i64, c_i64,
                                c_ptr, Strides, c_ptr]),
+    "hata_prefill_write": (c_i32, [c_ptr, c_ptr, Strides, c_ptr, c_ptr, Strides, c_i32, c_ptr, c_i32, c_i32, c_i32,
+                                   c_i32, c_i64, c_i64, c_i64, c_ptr, Strides, c_ptr]),
     "hata_append": (c_i32, [c_ptr, c_ptr, c_i32, c_ptr, c_ptr, c_ptr, Strides, c_ptr, Strides, c_ptr, c_i64, c_i32,
                             c_i32, c_i32, c_i32, c_ptr]),
     "hata_decode_topk_attn": (c_i32, [c_ptr, c_ptr, c_ptr, Strides, c_i32, c_ptr, Strides, c_ptr, c_i32, c_i32,

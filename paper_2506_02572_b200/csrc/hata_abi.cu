@@ -132,6 +132,27 @@ hata_status hata_hash_keys(const void* K, hata_strides ks, hata_dtype dt, const 
   return cuda_status(hata::launch_hash_keys_simt(p, dt == HATA_BF16, s));
 }
 
+hata_status hata_prefill_write(const void* K_src, const void* V_src, hata_strides ss, void* K, void* V,
+                               hata_strides kvs, hata_dtype dt, const void* W, int B, int H_kv, int d, int rbits,
+                               int64_t t0, int64_t n, int64_t cap, uint32_t* codes, hata_strides cs,
+                               hata_stream_t stream) {
+  if (!K_src || !V_src || !K || !V || !W || !codes || B < 1 || H_kv < 1 || rbits < 32 || rbits % 32 || t0 < 0 ||
+      n < 0 || !dtype_ok(dt))
+    return HATA_ERR_INVALID_ARG;
+  if (t0 + n > cap) return HATA_ERR_CAPACITY;
+  if (!shape_supported(d, rbits, 1) || dt != HATA_BF16) return HATA_ERR_UNSUPPORTED;
+  if (!kv_layout_ok(K, kvs, 2, d) || !kv_layout_ok(V, kvs, 2, d) || !kv_layout_ok(K_src, ss, 2, d) ||
+      !kv_layout_ok(V_src, ss, 2, d) || cs.st != rbits / 32 || !aligned(codes, 4) || !aligned(W, 16))
+    return HATA_ERR_INVALID_ARG;
+  if (n == 0) return HATA_OK;
+  hata::HashKeysParams p = {};
+  p.K = K; p.kv_sb = kvs.sb; p.kv_sh = kvs.sh; p.kv_st = kvs.st;
+  p.Wh = W; p.codes = codes; p.c_sb = cs.sb; p.c_sh = cs.sh;
+  p.t0 = t0; p.n = n; p.cap = cap; p.B = B; p.Hkv = H_kv; p.d = d; p.rbits = rbits;
+  return cuda_status(hata::launch_prefill_write_umma(p, K_src, V_src, ss.sb, ss.sh, ss.st, V,
+                                                     reinterpret_cast<cudaStream_t>(stream)));
+}
+
 hata_status hata_append(const void* k_new, const void* v_new, hata_dtype dt, const void* W, void* K, void* V,
                         hata_strides kvs, uint32_t* codes, hata_strides cs, const int64_t* pos, int64_t cap, int B,
                         int H_kv, int d, int rbits, hata_stream_t stream) {

@@ -23,6 +23,7 @@
 // N = rbits (32..256).  Synchronisation: mbarriers (TMA -> MMA full, MMA ->
 // TMA empty via tcgen05.commit, MMA -> epilogue accumulator full via
 // tcgen05.commit, epilogue -> MMA accumulator empty).
+#include <cstring>
 #include <cuda.h>                 // CUtensorMap (encoded through the runtime's driver entry point; no -lcuda)
 #include "hata_internal.h"
 #include "hata_common.cuh"
@@ -34,8 +35,8 @@ constexpr int UM_TOK = 128;                  // tokens per tile = UMMA M
 // epilogue warps: 4 (one per TMEM lane quadrant) x EPI_SPLIT column groups
 template <int N>
 constexpr int epi_split() { return N >= 64 ? 2 : 1; }
-template <int N>
-constexpr int um_threads() { return 64 + 128 * epi_split<N>(); }   // TMA warp, MMA warp, epilogue warps
+template <int N, bool F = false>
+constexpr int um_threads() { return 64 + 128 * epi_split<N>() + (F ? 32 : 0); }   // TMA, MMA, epilogue (+ store) warps
 constexpr int UM_SLAB = UM_TOK * 128;        // one [128 rows x 64 bf16] swizzled box (16 KB)
 
 // ---- tcgen05 / TMA primitives (inline PTX, sm_100a)
@@ -76,6 +77,19 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
       "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
       : "memory");
 }
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, int c0, int c1, int c2, const void* src) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.tile.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2)
+               : "memory");
+}
 // 32 lanes x 32 columns of 32-bit accumulators -> 32 registers per thread
 __device__ __forceinline__ void tmem_ld32_nowait(uint32_t taddr, uint32_t* v) {
   asm volatile(
@@ -93,32 +107,47 @@ template <int N>
 constexpr int tmem_cols() {                  // two accumulators, power of two >= 32
   return 2 * N <= 32 ? 32 : 2 * N <= 64 ? 64 : 2 * N <= 128 ? 128 : 2 * N <= 256 ? 256 : 512;
 }
-// K-tile ring depth: as many 32 KB stages as fit beside W_g^T (<= 6)
-template <int N>
+// bytes of one ring stage: the K tile (two swizzled slabs) [+ the V tile when
+// the prefill write is fused]
+template <bool F>
+constexpr int stage_bytes() { return 2 * UM_SLAB * (F ? 2 : 1); }
+// ring depth: as many stages as fit beside W_g^T (<= 6)
+template <int N, bool F = false>
 constexpr int um_stages() {
-  return (227 * 1024 - 1024 - 2 * N * 128 - 256) / (2 * UM_SLAB) > 6 ? 6 : (227 * 1024 - 1024 - 2 * N * 128 - 256) / (2 * UM_SLAB);
+  return (227 * 1024 - 1024 - 2 * N * 128 - 256) / stage_bytes<F>() > 6 ? 6
+                                                                        : (227 * 1024 - 1024 - 2 * N * 128 - 256) / stage_bytes<F>();
 }
-template <int N>
+template <int N, bool F = false>
 constexpr size_t umma_smem_bytes() {
-  return 1024 + (size_t)2 * N * 128 + (size_t)um_stages<N>() * 2 * UM_SLAB + 256;
+  return 1024 + (size_t)2 * N * 128 + (size_t)um_stages<N, F>() * stage_bytes<F>() + 256;
 }
 
-template <int N>
-__global__ void __launch_bounds__(um_threads<N>(), 1)
-    hash_keys_umma_kernel(const __grid_constant__ CUtensorMap tmK, const HashKeysParams p, int64_t row_sb,
-                          int64_t row_sh, int ntiles_unit, int tiles_per_cta) {
+// FUSED (NEXT-1, hata_prefill_write): the K tile comes from the new chunk
+// (3-D maps {d, token, unit}), the same smem tile is also stored to the K
+// cache and a V tile is carried through the stage to the V cache -- the keys
+// are read from HBM once for both the cache write and the hash.
+struct FusedMaps {
+  CUtensorMap Kd, Vs, Vd;   // K cache (store), V chunk (load), V cache (store)
+};
+
+template <int N, bool FUSED>
+__global__ void __launch_bounds__(um_threads<N, FUSED>(), 1)
+    hash_keys_umma_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ FusedMaps fm,
+                          const HashKeysParams p, int64_t row_sb, int64_t row_sh, int ntiles_unit, int tiles_per_cta) {
   constexpr int W = N / 32;
-  constexpr int UM_THREADS = um_threads<N>();
+  constexpr int UM_THREADS = um_threads<N, FUSED>();
   constexpr int ES = epi_split<N>();
   constexpr int WE = W / ES;                 // code words per epilogue thread
-  constexpr int UM_STAGES = um_stages<N>();
+  constexpr int UM_STAGES = um_stages<N, FUSED>();
+  constexpr int SB = stage_bytes<FUSED>();
+  constexpr int EPI_W0 = 2, EPI_W1 = 2 + 4 * ES;            // epilogue warps [EPI_W0, EPI_W1); store warp = EPI_W1
   constexpr uint32_t IDESC = idesc_bf16_f32(N);
   constexpr int BSLAB = N * 128;             // one [N x 64] swizzled slab of W_g^T
   extern __shared__ uint8_t smraw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
   uint8_t* Bs = sm;                                        // W_g^T, 2 slabs
   uint8_t* As = sm + 2 * BSLAB;                            // ring: UM_STAGES x 2 slabs
-  uint64_t* full = reinterpret_cast<uint64_t*>(As + UM_STAGES * 2 * UM_SLAB);
+  uint64_t* full = reinterpret_cast<uint64_t*>(As + UM_STAGES * SB);
   uint64_t* empty = full + UM_STAGES;
   uint64_t* tfull = empty + UM_STAGES;
   uint64_t* tempty = tfull + 2;
@@ -129,15 +158,24 @@ __global__ void __launch_bounds__(um_threads<N>(), 1)
   const int my_tiles = max(0, min(ntiles_unit, tile0 + tiles_per_cta) - tile0);
 
   const int64_t row_unit = (int64_t)b * row_sb + (int64_t)g * row_sh;   // tensor-map row of (b, g, t = 0)
-  auto produce = [&](int i) {                              // TMA: K tile i into stage i % UM_STAGES
+  auto produce = [&](int i) {                              // TMA: K (and V) tile i into stage i % UM_STAGES
     const int s = i % UM_STAGES;
-    const int row = (int)(row_unit + p.t0 + (int64_t)(tile0 + i) * UM_TOK);
-    mbar_arrive_expect_tx(&full[s], 2 * UM_SLAB);
-    tma_load_2d(As + s * 2 * UM_SLAB, &tmK, 0, row, &full[s]);
-    tma_load_2d(As + s * 2 * UM_SLAB + UM_SLAB, &tmK, 64, row, &full[s]);
+    mbar_arrive_expect_tx(&full[s], SB);
+    if constexpr (FUSED) {
+      const int tsrc = (tile0 + i) * UM_TOK;                 // chunk row
+      tma_load_3d(As + s * SB, &tmK, 0, tsrc, u, &full[s]);
+      tma_load_3d(As + s * SB + UM_SLAB, &tmK, 64, tsrc, u, &full[s]);
+      tma_load_3d(As + s * SB + 2 * UM_SLAB, &fm.Vs, 0, tsrc, u, &full[s]);
+    } else {
+      const int row = (int)(row_unit + p.t0 + (int64_t)(tile0 + i) * UM_TOK);
+      tma_load_2d(As + s * SB, &tmK, 0, row, &full[s]);
+      tma_load_2d(As + s * SB + UM_SLAB, &tmK, 64, row, &full[s]);
+    }
   };
   if (tid == 0) {
-    for (int s = 0; s < UM_STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    // a stage is free once its MMAs are done (tcgen05.commit) [and, fused,
+    // once the store warp's TMA stores have read it]
+    for (int s = 0; s < UM_STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], FUSED ? 2 : 1); }
     for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 4 * ES); }
     fence_mbar_init();
     // the first K tiles stream in while W_g^T is staged below
@@ -184,7 +222,7 @@ __global__ void __launch_bounds__(um_threads<N>(), 1)
         if (i >= 2) mbar_wait(&tempty[a], aph ^ 1u);       // epilogue drained accumulator a
         mbar_wait(&full[s], ph);                           // K tile landed
         tc_fence_after();
-        const uint32_t a_base = smem_u32(As + s * 2 * UM_SLAB), b_base = smem_u32(Bs);
+        const uint32_t a_base = smem_u32(As + s * SB), b_base = smem_u32(Bs);
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {                   // K = 128 = 8 x 16; 32-byte steps inside a swizzle atom
           const uint32_t ao = (uint32_t)((kk >> 2) * UM_SLAB + (kk & 3) * 32);
@@ -195,6 +233,21 @@ __global__ void __launch_bounds__(um_threads<N>(), 1)
         umma_commit(&empty[s]);                            // the stage is free once these MMAs are done
         umma_commit(&tfull[a]);                            // accumulator a is complete
       }
+    }
+  } else if (FUSED && warp == EPI_W1) {
+    if (lane == 0) {                                       // store warp: the landed K and V tiles -> the caches
+      for (int i = 0; i < my_tiles; ++i) {
+        const int s = i % UM_STAGES;
+        mbar_wait(&full[s], (uint32_t)(i / UM_STAGES) & 1u);
+        const int tdst = (int)(p.t0 + (int64_t)(tile0 + i) * UM_TOK);   // rows >= t0 + n are out of the maps' bounds
+        tma_store_3d(&fm.Kd, 0, tdst, u, As + s * SB);
+        tma_store_3d(&fm.Kd, 64, tdst, u, As + s * SB + UM_SLAB);
+        tma_store_3d(&fm.Vd, 0, tdst, u, As + s * SB + 2 * UM_SLAB);
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");   // the stage has been read
+        mbar_arrive(&empty[s]);
+      }
+      asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");           // writes complete before the trigger
     }
   } else {
     // epilogue: warp w >= 2 reads TMEM lane quadrant w % 4 (the lanes a warp
@@ -274,10 +327,12 @@ EncodeTiledFn encode_fn() {
   return fn;
 }
 
-template <int N>
-cudaError_t launch_n(const HashKeysParams& p, const CUtensorMap& map, int64_t row_sb, int64_t row_sh, cudaStream_t s) {
-  const size_t smem = umma_smem_bytes<N>();
-  cudaError_t e = cudaFuncSetAttribute(hash_keys_umma_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+template <int N, bool FUSED>
+cudaError_t launch_n(const HashKeysParams& p, const CUtensorMap& map, const FusedMaps& fm, int64_t row_sb,
+                     int64_t row_sh, cudaStream_t s) {
+  const size_t smem = umma_smem_bytes<N, FUSED>();
+  cudaError_t e = cudaFuncSetAttribute(hash_keys_umma_kernel<N, FUSED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem);
   if (e != cudaSuccess) return e;
   const int units = p.B * p.Hkv;
   const int ntiles = (int)((p.n + UM_TOK - 1) / UM_TOK);
@@ -286,8 +341,34 @@ cudaError_t launch_n(const HashKeysParams& p, const CUtensorMap& map, int64_t ro
   if (per_unit > ntiles) per_unit = ntiles;
   const int tiles_per_cta = (ntiles + per_unit - 1) / per_unit;
   const int nx = (ntiles + tiles_per_cta - 1) / tiles_per_cta;
-  hash_keys_umma_kernel<N><<<dim3(nx, units), um_threads<N>(), smem, s>>>(map, p, row_sb, row_sh, ntiles, tiles_per_cta);
+  hash_keys_umma_kernel<N, FUSED><<<dim3(nx, units), um_threads<N, FUSED>(), smem, s>>>(map, fm, p, row_sb, row_sh,
+                                                                                         ntiles, tiles_per_cta);
   return cudaGetLastError();
+}
+
+template <bool FUSED>
+cudaError_t dispatch_n(const HashKeysParams& p, const CUtensorMap& map, const FusedMaps& fm, int64_t row_sb,
+                       int64_t row_sh, cudaStream_t s) {
+  switch (p.rbits) {
+    case 32: return launch_n<32, FUSED>(p, map, fm, row_sb, row_sh, s);
+    case 64: return launch_n<64, FUSED>(p, map, fm, row_sb, row_sh, s);
+    case 128: return launch_n<128, FUSED>(p, map, fm, row_sb, row_sh, s);
+    case 256: return launch_n<256, FUSED>(p, map, fm, row_sb, row_sh, s);
+  }
+  return cudaErrorNotSupported;
+}
+
+// 3-D map {d, tokens, units} over a [B, H_kv, tokens, d] tensor whose batch
+// stride is H_kv times its head stride (one unit stride)
+bool map3d(EncodeTiledFn enc, CUtensorMap* m, const void* base, int64_t tokens, int units, int64_t st, int64_t sh,
+           bool swz) {
+  const cuuint64_t gdim[3] = {128, (cuuint64_t)tokens, (cuuint64_t)units};
+  const cuuint64_t gstride[2] = {(cuuint64_t)(st * 2), (cuuint64_t)(sh * 2)};
+  const cuuint32_t box[3] = {swz ? 64u : 128u, (cuuint32_t)UM_TOK, 1};
+  const cuuint32_t estride[3] = {1, 1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), gdim, gstride, box, estride,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, swz ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 }  // namespace
@@ -315,13 +396,34 @@ cudaError_t launch_hash_keys_umma(const HashKeysParams& p, cudaStream_t s) {
           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return cudaErrorNotSupported;
-  switch (p.rbits) {
-    case 32: return launch_n<32>(p, map, row_sb, row_sh, s);
-    case 64: return launch_n<64>(p, map, row_sb, row_sh, s);
-    case 128: return launch_n<128>(p, map, row_sb, row_sh, s);
-    case 256: return launch_n<256>(p, map, row_sb, row_sh, s);
-  }
-  return cudaErrorNotSupported;
+  FusedMaps none;
+  std::memset(&none, 0, sizeof(none));
+  return dispatch_n<false>(p, map, none, row_sb, row_sh, s);
+}
+
+// NEXT-1 (hata_prefill_write): rows [0, n) of the chunk K_src / V_src ->
+// rows [t0, t0 + n) of the K / V caches, and their codes, in one pass.
+cudaError_t launch_prefill_write_umma(const HashKeysParams& p, const void* Ksrc, const void* Vsrc, int64_t ss_b,
+                                      int64_t ss_h, int64_t ss_t, void* Vdst, cudaStream_t s) {
+  if (p.d != 128 || p.n <= 0) return p.n <= 0 ? cudaSuccess : cudaErrorNotSupported;
+  if (p.rbits != 32 && p.rbits != 64 && p.rbits != 128 && p.rbits != 256) return cudaErrorNotSupported;
+  auto al = [](const void* x) { return (reinterpret_cast<uintptr_t>(x) & 15) == 0; };
+  if (!al(Ksrc) || !al(Vsrc) || !al(p.K) || !al(Vdst) || (ss_t * 2) % 16 || (p.kv_st * 2) % 16 || (ss_h * 2) % 16 ||
+      (p.kv_sh * 2) % 16 || ss_b != (int64_t)p.Hkv * ss_h || p.kv_sb != (int64_t)p.Hkv * p.kv_sh || ss_t < 128 ||
+      p.kv_st < 128)
+    return cudaErrorNotSupported;
+  EncodeTiledFn enc = encode_fn();
+  if (!enc) return cudaErrorNotSupported;
+  const int units = p.B * p.Hkv;
+  CUtensorMap mk;
+  FusedMaps fm;
+  // destination maps end at row t0 + n of every unit: the tail tile's rows
+  // past it are clipped by the TMA store (never written)
+  if (!map3d(enc, &mk, Ksrc, p.n, units, ss_t, ss_h, true) || !map3d(enc, &fm.Vs, Vsrc, p.n, units, ss_t, ss_h, false) ||
+      !map3d(enc, &fm.Kd, p.K, p.t0 + p.n, units, p.kv_st, p.kv_sh, true) ||
+      !map3d(enc, &fm.Vd, Vdst, p.t0 + p.n, units, p.kv_st, p.kv_sh, false))
+    return cudaErrorNotSupported;
+  return dispatch_n<true>(p, mk, fm, 0, 0, s);
 }
 
 }  // namespace hata

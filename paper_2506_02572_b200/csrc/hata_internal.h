@@ -36,6 +36,10 @@ cudaError_t launch_hash_keys_simt(const HashKeysParams& p, int is_bf16, cudaStre
 // tcgen05/TMEM/TMA path (bf16, d == 128, rbits in {32, 64, 128, 256}, K strides
 // that one 2-D tensor map covers); cudaErrorNotSupported otherwise.
 cudaError_t launch_hash_keys_umma(const HashKeysParams& p, cudaStream_t s);
+// fused prefill write (NEXT-1): p.K = K cache, Vdst = V cache, source chunk
+// strides ss_*; cudaErrorNotSupported unless 3-D tensor maps cover both sides.
+cudaError_t launch_prefill_write_umma(const HashKeysParams& p, const void* Ksrc, const void* Vsrc, int64_t ss_b,
+                                      int64_t ss_h, int64_t ss_t, void* Vdst, cudaStream_t s);
 // legacy tensor-core path (mma.sync, bf16, d == 128): any strides.
 cudaError_t launch_hash_keys_tc(const HashKeysParams& p, cudaStream_t s);
 
