@@ -211,6 +211,9 @@ __device__ __forceinline__ unsigned atom_add_acq_rel_gpu(unsigned* p, unsigned v
   asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
   return old;
 }
+__device__ __forceinline__ void prefetch_l2_line(const void* g) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(g) : "memory");
+}
 __device__ __forceinline__ void prefetch_l2(const void* g, uint32_t bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(g), "r"(bytes) : "memory");
 }

@@ -191,6 +191,22 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
   if (warp == 0 && !ptab)                                           // the code chunk, a few large copies
     for (int s = 0; s < NST && s < nstages; ++s) issue_stage(s);
   for (int i = tid; i < p.nbins; i += DEC_THREADS) hist[i] = 0;
+  // L2 prefetch of the small inputs read right after the wait (q rows, new
+  // key/value rows, n[b], the unit's hint word): a prefetch only moves lines
+  // into L2, the point of coherence, so a value the preceding kernel writes
+  // is still read after the wait -- it just no longer waits for HBM
+  {
+    const int qlines = (G * D_HEAD * EB + 127) / 128;
+    if (tid < qlines) prefetch_l2_line(reinterpret_cast<const uint8_t*>(qg) + tid * 128);
+    else if (append && tid < qlines + 2 * ((D_HEAD * EB + 127) / 128)) {
+      const int i = tid - qlines, kl = (D_HEAD * EB + 127) / 128;
+      const void* src = i < kl ? p.k_new : p.v_new;
+      prefetch_l2_line(reinterpret_cast<const uint8_t*>(src) + (int64_t)u * D_HEAD * EB + (i % kl) * 128);
+    } else if (tid == DEC_THREADS - 1) {
+      prefetch_l2_line(p.n + b);
+      if (p.ws_sync) prefetch_l2_line(p.ws_sync + 4 * u);
+    }
+  }
   // Programmatic dependent launch: everything above reads only the hash
   // weights and code rows no preceding kernel writes (contract above); q,
   // k_new, v_new, n, K/V, the workspace and every global write come after
