@@ -268,6 +268,24 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
     __syncthreads();
   }
   HATA_TRACE(8);
+  // signed-weight planes of w_b = G - 2 c_b for code word w (hata_score.cuh):
+  // lane = bit of the word, c = #{h: q_h bit set}; P_j / N_j and this word's
+  // share of the constant K0 go to smem (whole warp)
+  const int sgn_s = (G % 2 == 0) ? 1 : 0;
+  auto word_planes = [&](int w, int c) {
+    const int v = (G - 2 * c) >> sgn_s;                              // exact: G - 2c is even for even G
+    const int mag = v < 0 ? -v : v;
+    int negc = 0;
+#pragma unroll
+    for (int j = 0; j < J; ++j) {
+      const uint32_t pj = __ballot_sync(0xffffffffu, v > 0 && ((mag >> j) & 1));
+      const uint32_t nj = __ballot_sync(0xffffffffu, v < 0 && ((mag >> j) & 1));
+      negc += __popc(nj) << j;
+      if (lane == 0) { planes[j * 8 + w] = pj; planes[32 + j * 8 + w] = nj; }
+    }
+    const int csum = warp_sum_i(c);
+    if (lane == 0) reinterpret_cast<int*>(planes)[64 + w] = csum - (negc << sgn_s);   // K0 share of this word
+  };
   if constexpr (EB == 2) {
     // bf16: the projection X[NV x d] . W_g[d x rbits] on the tensor cores
     // (mma.sync m16n8k16, exact bf16 products, fp32 accumulation; R13).
@@ -314,6 +332,15 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
         if (gid < NV) qw[gid * W + w] = lo;
         if (gid + 8 < NV) qw[(gid + 8) * W + w] = hi;
       }
+      // the G query words of this code word are in lanes 0, 4, .. (rows = heads
+      // < 8): the planes follow in-warp, no smem round trip
+      int cnt = 0;
+#pragma unroll
+      for (int h = 0; h < GT; ++h) {
+        const uint32_t wh = __shfl_sync(0xffffffffu, lo, 4 * h);
+        if (h < G) cnt += (wh >> lane) & 1u;
+      }
+      word_planes(w, cnt);
     }
   } else {
     // fp32: thread = (bit, j-slice), all vectors at once (fp32 FMA; slices
@@ -364,27 +391,15 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
     if (h < G && p.out_qcodes && r == 0) p.out_qcodes[((int64_t)b * p.Hq + g * G + h) * W + w] = word;
     if (h == G) const_cast<uint32_t*>(p.codes)[cmap(pos) + w] = word;
   }
-  // signed-weight planes of w_b = G - 2 c_b, c_b = #{h: q_h bit b set}
-  // (hata_score.cuh): P_j / N_j and the constant K0, one warp per code word
-  const int sgn_s = (G % 2 == 0) ? 1 : 0;
-  if (warp < W) {
-    int c = 0;
-    for (int h = 0; h < G; ++h) c += (qw[h * W + warp] >> lane) & 1u;
-    const int v = (G - 2 * c) >> sgn_s;                              // exact: G - 2c is even for even G
-    const int mag = v < 0 ? -v : v;
-    int negc = 0;
-#pragma unroll
-    for (int j = 0; j < J; ++j) {
-      const uint32_t pj = __ballot_sync(0xffffffffu, v > 0 && ((mag >> j) & 1));
-      const uint32_t nj = __ballot_sync(0xffffffffu, v < 0 && ((mag >> j) & 1));
-      negc += __popc(nj) << j;
-      if (lane == 0) { planes[j * 8 + warp] = pj; planes[32 + j * 8 + warp] = nj; }
+  if constexpr (EB != 2) {                                          // fp32: planes from the smem words
+    if (warp < W) {
+      int c = 0;
+      for (int h = 0; h < G; ++h) c += (qw[h * W + warp] >> lane) & 1u;
+      word_planes(warp, c);
     }
-    const int csum = warp_sum_i(c);
-    if (lane == 0) reinterpret_cast<int*>(planes)[64 + warp] = csum - (negc << sgn_s);   // K0 share of this word
+    __syncthreads();
   }
   HATA_TRACE(26);
-  __syncthreads();
   uint32_t A[J][W], Bp[J][W];                                       // P_j, N_j
 #pragma unroll
   for (int j = 0; j < J; ++j)
