@@ -136,9 +136,9 @@ DecodePlan plan_decode(int B, int Hq, int Hkv, int d, int rbits, int64_t n_max, 
   // n_max (hence M) and k change; the sections after it are fully written
   // before they are read in a launch.
   size_t off = 0;
-  pl.ws_sync = off;  off += up256((size_t)units * 4 * 4);          // [2] = threshold hint (any M)
-  pl.ws_hist = off;  off += M > 1 ? up256((size_t)units * M * hs * 4) : 0;
-  pl.ws_part = off;  off += M > 1 ? up256((size_t)units * M * dec_part_stride(GT, d) * 4) : 0;
+  pl.ws_sync = off;  off += up256((size_t)units * 4 * 4);          // epoch, hint slots (any M)
+  pl.ws_hist = off;  off += M > 1 ? up256((size_t)units * M * hs * 8) : 0;          // tagged words
+  pl.ws_part = off;  off += M > 1 ? up256((size_t)units * M * dec_part_stride(GT, d) * 8) : 0;
   pl.ws_D = off;     off += !pl.d_smem ? up256((size_t)units * M * dec_dchunk(pl.chunk) * 2) : 0;
   pl.ws_rows = off;  off += pl.rows_global ? up256((size_t)units * M * pl.R_cap * 4) : 0;
   pl.ws_total = off;
@@ -159,8 +159,8 @@ cudaError_t launch_decode(DecodeParams& p, const DecodePlan& pl, void* ws, int i
   p.M = pl.M; p.stages = pl.stages; p.chunk = pl.chunk; p.nbins = pl.nbins; p.rows_cap = pl.rows_cap; p.R_cap = pl.R_cap;
   p.d_smem = pl.d_smem;
   p.ws_sync = reinterpret_cast<unsigned*>(w + pl.ws_sync);
-  p.ws_hist = pl.M > 1 ? reinterpret_cast<int32_t*>(w + pl.ws_hist) : nullptr;
-  p.ws_part = pl.M > 1 ? reinterpret_cast<float*>(w + pl.ws_part) : nullptr;
+  p.ws_hist = pl.M > 1 ? reinterpret_cast<uint64_t*>(w + pl.ws_hist) : nullptr;
+  p.ws_part = pl.M > 1 ? reinterpret_cast<uint64_t*>(w + pl.ws_part) : nullptr;
   p.ws_D = !pl.d_smem ? reinterpret_cast<uint16_t*>(w + pl.ws_D) : nullptr;
   p.ws_rows = pl.rows_global ? reinterpret_cast<int32_t*>(w + pl.ws_rows) : nullptr;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, pl.smem);

@@ -80,10 +80,12 @@ struct DecodeParams {
   int32_t* ws_rows;        // [units, M, R_cap] rows list when it does not fit in smem, else null
   int d_smem;              // 1: this rank's D lives in smem, else in ws_D
   // workspace (global); zero-initialised once, left zeroed by every launch
-  int32_t* ws_hist;        // [units, M, hs] exclusive prefix counts cum_r[0..nbins]   (M > 1)
+  // tagged words (tag << 32 | 32-bit value): tag = this launch's epoch, so a
+  // reader that sees the tag sees the value -- no fences, no arrival counters
+  uint64_t* ws_hist;       // [units, M, hs] exclusive prefix counts cum_r[0..nbins]   (M > 1)
   uint16_t* ws_D;          // [units, M, chunk] D when it does not fit in smem (!d_smem)
-  float* ws_part;          // [units, M, GT, d+2]          (M > 1)
-  unsigned* ws_sync;       // [units, 4]: barrier, done (M > 1), threshold hint, hint-use counters
+  uint64_t* ws_part;       // [units, M, GT, d+2] float bits  (M > 1)
+  unsigned* ws_sync;       // [units, 4]: epoch, threshold hint (2 slots by epoch parity), hint-use counters
   // sequence-shard phase 1 (hata_shard_candidates): stop after the select and
   // emit (D, global index) candidates instead of attending.
   int cand_mode;
@@ -201,6 +203,16 @@ __device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+// 64-bit tagged words of the exchange / merge (single-copy atomic when aligned)
+__device__ __forceinline__ uint64_t ld_relaxed_u64(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed_u64(uint64_t* p, uint64_t v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t tag_of(uint64_t v) { return (uint32_t)(v >> 32); }
 // Release-add without a return value (arrival at a barrier counter).
 __device__ __forceinline__ void red_add_release_gpu(unsigned* p, unsigned v) {
   asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");

@@ -10,7 +10,8 @@
 //      unit's ranks, threshold + tie quotas, order-preserving compaction of
 //      this rank's equal share of the selection        Alg. 3 lines 12-13
 //   4  gather-fused softmax attention over that share Alg. 3 lines 14-17
-//   5  rank-ordered flash-decoding merge by the last rank to finish
+//   5  rank-ordered flash-decoding merge of the epoch-tagged partials by
+//      min(G, M) merger ranks (one or more heads each)
 #pragma once
 #include <type_traits>
 #include "hata_attn_mma.cuh"
@@ -228,7 +229,14 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
                              : reinterpret_cast<const T*>(row == G ? p.k_new : p.v_new) + (int64_t)u * D_HEAD;
       dq[i] = __ldcg(reinterpret_cast<const uint4*>(src) + c);
     }
-    if (tid == 0) misc[14] = p.ws_sync ? (int)__ldcg(p.ws_sync + 4 * u + 2) : 0;
+    if (tid == 0) {
+      // the unit's sync words in one load: epoch E (this launch tags its
+      // exchange and partials with E + 1), the threshold hint of launch E in
+      // slot 1 + (E & 1) (launch E + 1 writes the other slot)
+      const uint4 sw = p.ws_sync ? __ldcg(reinterpret_cast<const uint4*>(p.ws_sync + 4 * u)) : make_uint4(0, 0, 0, 0);
+      misc[12] = (int)(sw.x + 1u);
+      misc[14] = (int)((sw.x & 1u) ? sw.z : sw.y);
+    }
     if (warp == 0 && ptab)                                          // paged: the page table is read after the wait
       for (int s = 0; s < NST && s < nstages; ++s) issue_stage(s);
   }
@@ -262,6 +270,8 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
   // exchange reads every rank's prefix counts at the window [hw0, hw0 + DEC_WIN)
   int hw0 = 0;
   if (hinted) { const int h = misc[14]; Th = h > 0 ? h + DEC_HINT_SLACK : -1; hw0 = h - (DEC_WIN / 2 - 1); }
+  const uint32_t tag = (uint32_t)misc[12];                          // this launch's epoch tag (>= 1)
+  const uint64_t tagw = (uint64_t)tag << 32;
   HATA_TRACE(9);
   if constexpr (EB != 2) {                                          // fp32 paths read q as floats
     for (int i = tid; i < NV * D_HEAD; i += DEC_THREADS) qf[(i / D_HEAD) * QS + i % D_HEAD] = Elem<T>::to_f(qraw[i]);
@@ -552,13 +562,13 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
   // thr = D of the k'-th best token; every D < thr is selected; ties at thr
   // are taken lowest index first (R8): rank by rank (= token order), and in
   // token order inside a rank.  Every rank publishes the exclusive prefix
-  // counts of its D histogram (cum_r[i] = #{local D < i}, i = 0..nbins) and
-  // adds them into the unit total; after ONE barrier each rank reads the
-  // total (-> thr) and the other ranks' cum_r[thr], cum_r[thr+1] (-> its tie
-  // quota and the output position of its first selected token), then
-  // compacts its OWN selected tokens in order and attends to them.
+  // counts of its D histogram (cum_r[i] = #{local D < i}, i = 0..nbins) as
+  // epoch-tagged words; each rank polls the M ranks' words (the window
+  // around the hint, else every bin) -> the unit totals (-> thr) and the
+  // ranks' cum_r[thr], cum_r[thr+1] (-> its tie quota and the output
+  // position of its first selected token), then compacts its OWN selected
+  // tokens in order and attends to them.
   const int hs = dec_hist_stride(p.nbins + 1);
-  unsigned* sync = (M > 1) ? p.ws_sync + 4 * u : nullptr;
   HATA_TRACE(2);
   constexpr int BPT_MAX = (8 * 256 + 1 + DEC_THREADS) / DEC_THREADS;  // nbins + 1 <= G*rbits + 2 (G <= 8, rbits <= 256)
   const int BPT = (p.nbins + DEC_THREADS) / DEC_THREADS;
@@ -599,39 +609,57 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
     }
   };
   if (M > 1) {
-    // publish this rank's prefix counts (plain stores), arrive
-    int32_t* gc = p.ws_hist + ((int64_t)u * M + r) * hs;
-    const int32_t* gu = p.ws_hist + (int64_t)u * M * hs;           // rank rr's counts: gu + rr * hs
+    // publish this rank's prefix counts as tagged words: no fence and no
+    // arrival counter -- a reader that sees this launch's tag sees the count
+    uint64_t* gc = p.ws_hist + ((int64_t)u * M + r) * hs;
+    const uint64_t* gu = p.ws_hist + (int64_t)u * M * hs;          // rank rr's counts: gu + rr * hs
     int c = cum;
 #pragma unroll
     for (int q = 0; q < BPT_MAX; ++q) {
       const int i = i0 + q;
-      if (q < BPT && i <= p.nbins) gc[i] = c;
+      if (q < BPT && i <= p.nbins) st_relaxed_u64(gc + i, tagw | (uint32_t)c);
       c += tb[q];
     }
-    __syncthreads();
-    if (tid == 0) red_add_release_gpu(sync, 1u);   // release the CTA's writes (cumulative over bar.sync)
     build_bitmap();
     HATA_TRACE(27);
-    if (tid == 0) {
-      for (unsigned spins = 0; ld_acquire_gpu(sync) < (unsigned)M;)
-        if (++spins > HATA_SPIN_LIMIT) __trap();                     // a lost arrival: fail loudly, never hang
-      // the owner's K/V row (generic stores) -> this CTA's gather (async proxy)
-      asm volatile("fence.proxy.async.global;" ::: "memory");
+    // the owner's K/V row (generic stores) -> this CTA's gather (async proxy)
+    if (tid == 0) asm volatile("fence.proxy.async.global;" ::: "memory");
+    // with a hint, every rank's prefix counts at the window bins
+    // [w0, w0 + DEC_WIN) around it, polled until each word carries this
+    // launch's tag (all of a thread's words in flight at once): the unit
+    // totals there give the threshold when it falls in the window, and the
+    // per-rank values the tie quota -- one round trip after the last rank
+    // publishes
+    const int w0 = hw0;
+    if (Th >= 0) {
+      constexpr int WJ = (DEC_MAX_RANKS * DEC_WIN + DEC_THREADS - 1) / DEC_THREADS;
+      uint32_t pend = 0u;
+#pragma unroll
+      for (int j = 0; j < WJ; ++j) {
+        const int i = tid + j * DEC_THREADS, bi = w0 + i % DEC_WIN;
+        if (i < M * DEC_WIN) {
+          if (bi >= 0 && bi <= p.nbins) pend |= 1u << j;
+          else win[i] = 0;
+        }
+      }
+      for (unsigned spins = 0; pend;) {
+        uint64_t x[WJ];
+#pragma unroll
+        for (int j = 0; j < WJ; ++j) {
+          const int i = tid + j * DEC_THREADS;
+          if ((pend >> j) & 1u) x[j] = ld_relaxed_u64(gu + (int64_t)(i / DEC_WIN) * hs + w0 + i % DEC_WIN);
+        }
+#pragma unroll
+        for (int j = 0; j < WJ; ++j)
+          if (((pend >> j) & 1u) && tag_of(x[j]) == tag) {
+            win[tid + j * DEC_THREADS] = (int)(uint32_t)x[j];
+            pend &= ~(1u << j);
+          }
+        if (pend && ++spins > HATA_SPIN_LIMIT) __trap();           // a lost rank: fail loudly, never hang
+      }
     }
     __syncthreads();
     HATA_TRACE(3);
-    // with a hint, every rank's prefix counts at the window bins
-    // [w0, w0 + DEC_WIN) around it: the unit totals there give the threshold
-    // when it falls in the window, and the per-rank values the tie quota --
-    // one round trip, no unit-total atomics
-    const int w0 = hw0;
-    if (Th >= 0)
-      for (int i = tid; i < M * DEC_WIN; i += DEC_THREADS) {
-        const int rr = i / DEC_WIN, bi = w0 + i % DEC_WIN;
-        win[i] = (bi >= 0 && bi <= p.nbins) ? __ldcg(gu + (int64_t)rr * hs + bi) : 0;
-      }
-    __syncthreads();
     static_assert(DEC_WIN == 32, "one lane per window bin");
     if (warp == 0) {
       int tot = 0;
@@ -645,18 +673,28 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
       if (lane == 0) misc[5] = any ? 1 : 0;
     }
     __syncthreads();
-    if (!misc[5] && kp > 0) {
+    if (!misc[5] && (kp > 0 || r == 0)) {
       // no hint, or the threshold is outside the window: unit totals of
-      // every bin from the M ranks' published prefix counts -- thread per
-      // bin, all M loads in flight (one round trip), totals in the code
-      // ring (free after scoring), then the crossing bin
+      // every bin from the M ranks' tagged prefix counts -- thread per bin,
+      // all M words in flight per poll (one round trip), totals in the code
+      // ring (free after scoring), then the crossing bin.  (Rank 0 also
+      // runs it when k' = 0: it must have seen every rank's words before it
+      // advances the epoch.)
       int32_t* tots = reinterpret_cast<int32_t*>(ring);
+      const uint32_t all = M >= 32 ? 0xffffffffu : (1u << M) - 1u;
       for (int j = tid; j <= p.nbins; j += DEC_THREADS) {
-        int t8[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        int tot = 0;
+        for (uint32_t pend = all, spins = 0; pend;) {
+          uint64_t x[DEC_MAX_RANKS];
 #pragma unroll
-        for (int rr = 0; rr < DEC_MAX_RANKS; ++rr)
-          if (rr < M) t8[rr & 7] += __ldcg(gu + (int64_t)rr * hs + j);
-        tots[j] = ((t8[0] + t8[1]) + (t8[2] + t8[3])) + ((t8[4] + t8[5]) + (t8[6] + t8[7]));
+          for (int rr = 0; rr < DEC_MAX_RANKS; ++rr)
+            if ((pend >> rr) & 1u) x[rr] = ld_relaxed_u64(gu + (int64_t)rr * hs + j);
+#pragma unroll
+          for (int rr = 0; rr < DEC_MAX_RANKS; ++rr)
+            if (((pend >> rr) & 1u) && tag_of(x[rr]) == tag) { tot += (int)(uint32_t)x[rr]; pend &= ~(1u << rr); }
+          if (pend && ++spins > HATA_SPIN_LIMIT) __trap();
+        }
+        tots[j] = tot;
       }
       __syncthreads();
       for (int j = tid; j < p.nbins; j += DEC_THREADS) {
@@ -677,7 +715,7 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
   __syncthreads();
   const int thr = misc[0];
   const int need = misc[1];
-  if (p.ws_sync && r == 0 && tid == 0) reinterpret_cast<int*>(p.ws_sync)[4 * u + 2] = thr;   // next launch's hint
+  if (p.ws_sync && r == 0 && tid == 0) reinterpret_cast<int*>(p.ws_sync)[4 * u + 1 + (tag & 1u)] = thr;   // launch E+1's hint slot
   // this rank's tie quota and the selection position of its first token
   // (computed by every warp: no further barrier); the loads are issued here
   // and consumed after the counting pass below
@@ -689,9 +727,13 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
       bl = win[lane * DEC_WIN + thr - w0];
       ti = win[lane * DEC_WIN + thr + 1 - w0];
     } else {
-      const int32_t* cr = p.ws_hist + ((int64_t)u * M + lane) * hs;
-      bl = __ldcg(cr + thr);
-      ti = __ldcg(cr + thr + 1);
+      // outside the window: rank `lane`'s tagged prefix counts at thr, thr + 1
+      const uint64_t* cr = p.ws_hist + ((int64_t)u * M + lane) * hs;
+      for (unsigned spins = 0;;) {
+        const uint64_t x0 = ld_relaxed_u64(cr + thr), x1 = ld_relaxed_u64(cr + thr + 1);
+        if (tag_of(x0) == tag && tag_of(x1) == tag) { bl = (int)(uint32_t)x0; ti = (int)(uint32_t)x1; break; }
+        if (++spins > HATA_SPIN_LIMIT) __trap();
+      }
     }
   }
   HATA_TRACE(11);
@@ -953,62 +995,92 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
         }
       }
     }
+    if (p.ws_sync && tid == 0) p.ws_sync[4 * u] = tag;              // advance the unit's epoch
     HATA_TRACE(7);
     return;
   }
+  // every rank publishes its partial (m, l, acc) as tagged words and is done:
+  // no fence, no arrival counter -- ranks >= nmerge exit at once (their SMs
+  // go to the next launch); merger rank j < nmerge = min(G, M) polls the
+  // words of heads j, j + nmerge, .. until every one carries this launch's
+  // tag and merges them in rank order (G mergers: each pulls 1/G of the
+  // partial bytes into its SM)
   const int PS = D_HEAD + 2;
   const int PB = dec_part_stride(GT, D_HEAD);
-  float* mypart = p.ws_part + ((int64_t)u * M + r) * PB;
   if (!cand_mode) {
+    uint64_t* mypart = p.ws_part + ((int64_t)u * M + r) * PB;
 #pragma unroll
     for (int s = 0; s < NSL; ++s) {
       const int sl = tid + s * DEC_THREADS;
       const int h = sl / (D_HEAD / 2), e2 = sl % (D_HEAD / 2);
-      if (h < G) *reinterpret_cast<float2*>(mypart + h * PS + 2 + 2 * e2) = make_float2(st.acc[s][0], st.acc[s][1]);
+      if (h < G) {
+        st_relaxed_u64(mypart + h * PS + 2 + 2 * e2, tagw | __float_as_uint(st.acc[s][0]));
+        st_relaxed_u64(mypart + h * PS + 3 + 2 * e2, tagw | __float_as_uint(st.acc[s][1]));
+      }
     }
-    if (tid < G) { mypart[tid * PS] = m_s[tid]; mypart[tid * PS + 1] = l_s[tid]; }
+    if (tid < G) {
+      st_relaxed_u64(mypart + tid * PS, tagw | __float_as_uint(m_s[tid]));
+      st_relaxed_u64(mypart + tid * PS + 1, tagw | __float_as_uint(l_s[tid]));
+    }
   }
-  __syncthreads();
   HATA_CLK(8);
-  // ranks 1..M-1 release their partial (cumulative over bar.sync) and exit
-  // at once (their SMs go to the next launch); rank 0 waits for them and merges
-  if (r != 0) {
-    if (tid == 0) red_add_release_gpu(sync + 1, 1u);
+  const int nmerge = cand_mode ? 1 : min(G, M);
+  if (r >= nmerge) {
     HATA_TRACE(15);
     return;
   }
-  if (tid == 0) {
-    for (unsigned spins = 0; ld_acquire_gpu(sync + 1) < (unsigned)(M - 1);)
-      if (++spins > HATA_SPIN_LIMIT) __trap();
-  }
-  HATA_CLK(9);
-  __syncthreads();
   HATA_TRACE(15);
-  // rank 0: every partial is visible (writer release + counter); merge them
-  // in rank order straight from L2 (thread = one output element)
   if (!cand_mode) {
-    // merge weights once per head: warp h (< G) holds rank r in lane r,
-    // w[r][h] = e^{m_r - M_h} and 1 / L_h go to smem; every output thread
-    // issues its M partial loads up front (one L2 round trip)
-    const float* part = p.ws_part + (int64_t)u * M * PB;
+    // merger r: heads h = r + nmerge * hi, hi < nh.  Warp hi holds rank i in
+    // lane i: w[i][hi] = e^{m_i - M_h} and 1 / L_h go to smem; every output
+    // thread polls its M partial words (all in flight per poll)
+    const uint64_t* part = p.ws_part + (int64_t)u * M * PB;
     float* wts = reinterpret_cast<float*>(smem + L.ring);             // [DEC_MAX_RANKS][GT] + [GT] (ring is free)
     float* linv = wts + DEC_MAX_RANKS * GT;
-    constexpr int NO = (GT * D_HEAD + DEC_THREADS - 1) / DEC_THREADS;   // outputs per thread
+    const int nh = (G - r + nmerge - 1) / nmerge;                     // heads of this merger
+    constexpr int NO = (GT * D_HEAD + DEC_THREADS - 1) / DEC_THREADS;   // outputs per thread (bound)
     constexpr int OB = NO < 2 ? NO : 2;                                  // outputs per pass (registers)
+    const uint32_t all = M >= 32 ? 0xffffffffu : (1u << M) - 1u;
     float v[OB][DEC_MAX_RANKS];
-    auto load_pass = [&](int ob) {
+    auto poll_pass = [&](int ob) {
+      uint32_t pend[OB];
 #pragma unroll
       for (int q = 0; q < OB; ++q) {
-        const int o = tid + (ob + q) * DEC_THREADS, h = o / D_HEAD, e = o % D_HEAD;
-        const bool ok = ob + q < NO && h < G;
+        const int o = tid + (ob + q) * DEC_THREADS;
+        pend[q] = (ob + q < NO && o < nh * D_HEAD) ? all : 0u;
+      }
+      for (unsigned spins = 0;;) {
+        uint32_t any = 0u;
 #pragma unroll
-        for (int i = 0; i < DEC_MAX_RANKS; ++i) v[q][i] = ok && i < M ? __ldcg(part + i * PB + h * PS + 2 + e) : 0.f;
+        for (int q = 0; q < OB; ++q) any |= pend[q];
+        if (!any) break;
+        if (++spins > HATA_SPIN_LIMIT) __trap();
+#pragma unroll
+        for (int q = 0; q < OB; ++q) {
+          const int o = tid + (ob + q) * DEC_THREADS, h = r + nmerge * (o / D_HEAD), e = o % D_HEAD;
+          uint64_t x[DEC_MAX_RANKS];
+#pragma unroll
+          for (int i = 0; i < DEC_MAX_RANKS; ++i)
+            if ((pend[q] >> i) & 1u) x[i] = ld_relaxed_u64(part + i * PB + h * PS + 2 + e);
+#pragma unroll
+          for (int i = 0; i < DEC_MAX_RANKS; ++i)
+            if (((pend[q] >> i) & 1u) && tag_of(x[i]) == tag) {
+              v[q][i] = __uint_as_float((uint32_t)x[i]);
+              pend[q] &= ~(1u << i);
+            }
+        }
       }
     };
-    load_pass(0);
-    if (warp < G) {
-      const float mr = lane < M ? __ldcg(part + lane * PB + warp * PS) : -INFINITY;
-      const float lr = lane < M ? __ldcg(part + lane * PB + warp * PS + 1) : 0.f;
+    if (warp < nh) {
+      // rank `lane`'s (m, l) of head h
+      const int h = r + nmerge * warp;
+      float mr = -INFINITY, lr = 0.f;
+      if (lane < M)
+        for (unsigned spins = 0;;) {
+          const uint64_t xm = ld_relaxed_u64(part + lane * PB + h * PS), xl = ld_relaxed_u64(part + lane * PB + h * PS + 1);
+          if (tag_of(xm) == tag && tag_of(xl) == tag) { mr = __uint_as_float((uint32_t)xm); lr = __uint_as_float((uint32_t)xl); break; }
+          if (++spins > HATA_SPIN_LIMIT) __trap();
+        }
       float Mx = mr;
 #pragma unroll
       for (int x = 16; x > 0; x >>= 1) Mx = fmaxf(Mx, __shfl_xor_sync(0xffffffffu, Mx, x));
@@ -1019,23 +1091,32 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
       if (lane < DEC_MAX_RANKS) wts[lane * GT + warp] = w;
       if (lane == 0) linv[warp] = Ls > 0.f ? 1.f / Ls : 0.f;
     }
+    poll_pass(0);
     __syncthreads();
+    HATA_TRACE(14);
     for (int ob = 0; ob < NO; ob += OB) {
-      if (ob) load_pass(ob);
+      if (ob) poll_pass(ob);
 #pragma unroll
       for (int q = 0; q < OB; ++q) {
-        const int o = tid + (ob + q) * DEC_THREADS, h = o / D_HEAD, e = o % D_HEAD;
-        if (ob + q < NO && h < G) {
+        const int o = tid + (ob + q) * DEC_THREADS, hi = o / D_HEAD, e = o % D_HEAD;
+        if (ob + q < NO && o < nh * D_HEAD) {
           float a0 = 0.f;
 #pragma unroll
-          for (int i = 0; i < DEC_MAX_RANKS; ++i) a0 = fmaf(v[q][i], wts[i * GT + h], a0);   // rank order
-          store_out(h, e, a0 * linv[h]);
+          for (int i = 0; i < DEC_MAX_RANKS; ++i)
+            if (i < M) a0 = fmaf(v[q][i], wts[i * GT + hi], a0);       // rank order
+          store_out(r + nmerge * hi, e, a0 * linv[hi]);
         }
       }
     }
+  } else {
+    // candidates only: rank 0 has polled every rank's prefix counts (the
+    // exchange) before it advances the epoch below
   }
   HATA_CLK(10);
-  if (tid == 0) { sync[0] = 0u; sync[1] = 0u; }
+  // advance the unit's epoch: rank 0 has seen a tagged word of every rank
+  // (its partials, or in candidates mode the exchange), so every CTA of this
+  // launch has read the old epoch
+  if (r == 0 && tid == 0) p.ws_sync[4 * u] = tag;
   HATA_TRACE(7);
   HATA_CLK(14);
 }

@@ -19,7 +19,7 @@ import synth  # noqa: E402
 
 NAMES = {31: "kernel_entry", 0: "start", 1: "hash_done", 2: "score_done", 3: "hist_x", 4: "D_staged", 5: "select_done",
          6: "attn_done", 7: "end(last)", 8: "qk_loaded", 9: "W_ready", 10: "stage0", 11: "thr",
-         12: "quota", 13: "last_stage", 14: "sel_pass1_done", 15: "published", 16: "kv_gathered",
+         12: "quota", 13: "last_stage", 14: "merge_polled", 15: "published", 16: "kv_gathered",
          17: "groups_done", 19: "kv_issued", 20: "kv_gathered_1st", 21: "groups_done_1st",
          23: "kv_issued_1st", 20: "attn_entry", 27: "arrived", 28: "wait_done", 18: "sel_counted", 21: "sel_scanned", 22: "sel_emitted", 29: "attn_wmerge1", 30: "attn_wmerge2", 24: "hash_mma_done(t0)", 25: "hash_synced", 26: "planes_done(t0)"}
 
