@@ -135,10 +135,16 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
 }
-constexpr int HATA_TRACE_SLOTS = 64;   // [0, 32) %globaltimer stamps, [32, 64) clock64 stamps
+constexpr int HATA_TRACE_SLOTS = 96;   // [0, 32) %globaltimer stamps, [32, 64) clock64 stamps (HATA_CLK),
+                                       // [64, 96) clock64 at the %globaltimer stamps
 __device__ __forceinline__ void trace_at(unsigned long long* tr, int i) {
-  if (tr != nullptr && threadIdx.x == 0)
-    tr[((size_t)blockIdx.y * gridDim.x + blockIdx.x) * HATA_TRACE_SLOTS + i] = globaltimer_ns();
+  if (tr != nullptr && threadIdx.x == 0) {
+    unsigned long long c;
+    asm volatile("mov.u64 %0, %%clock64;" : "=l"(c)::"memory");
+    const size_t base = ((size_t)blockIdx.y * gridDim.x + blockIdx.x) * HATA_TRACE_SLOTS;
+    tr[base + i] = globaltimer_ns();
+    tr[base + 64 + i] = c;
+  }
 }
 __device__ __forceinline__ void clock_at(unsigned long long* tr, int i) {
   if (tr != nullptr && threadIdx.x == 0) {

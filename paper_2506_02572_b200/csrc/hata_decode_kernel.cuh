@@ -663,8 +663,10 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
     static_assert(DEC_WIN == 32, "one lane per window bin");
     if (warp == 0) {
       int tot = 0;
-      if (Th >= 0)
+      if (Th >= 0) {
+#pragma unroll 8
         for (int rr = 0; rr < M; ++rr) tot += win[rr * DEC_WIN + lane];
+      }
       const int z = __shfl_down_sync(0xffffffffu, tot, 1);
       const int bj = w0 + lane;                                       // bins bj, bj + 1 both in the window
       const bool hit = Th >= 0 && lane < DEC_WIN - 1 && bj >= 0 && bj + 1 <= p.nbins && kp > 0 && tot < kp && kp <= z;
@@ -930,6 +932,9 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
   }
   HATA_CLK(6);
   HATA_TRACE(22);
+#if HATA_DIAG
+  if (p.trace && tid == 0) p.trace[((size_t)blockIdx.y * gridDim.x + blockIdx.x) * HATA_TRACE_SLOTS + 32 + 15] = (unsigned long long)Rr;
+#endif
   if (r == 0) {
     for (int i = kp + tid; i < p.k; i += DEC_THREADS) {
       if (oidx) oidx[i] = -1;
@@ -1031,56 +1036,55 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
   }
   HATA_TRACE(15);
   if (!cand_mode) {
-    // merger r: heads h = r + nmerge * hi, hi < nh.  Warp hi holds rank i in
-    // lane i: w[i][hi] = e^{m_i - M_h} and 1 / L_h go to smem; every output
-    // thread polls its M partial words (all in flight per poll)
+    // merger r: heads h = r + nmerge * hi, hi < nh.  The (rank i, head hi)
+    // partial rows -- pairs -- are polled warp by warp (warp w: pairs w,
+    // w + DEC_WARPS, ..; lane: words lane, lane + 32, .. of the row), every
+    // word of a lane in flight per poll, into smem; then warp hi computes
+    // the merge weights w[i][hi] = e^{m_i - M_h} and 1 / L_h, and thread
+    // (hi, e) sums the M ranks' acc in rank order
     const uint64_t* part = p.ws_part + (int64_t)u * M * PB;
-    float* wts = reinterpret_cast<float*>(smem + L.ring);             // [DEC_MAX_RANKS][GT] + [GT] (ring is free)
-    float* linv = wts + DEC_MAX_RANKS * GT;
     const int nh = (G - r + nmerge - 1) / nmerge;                     // heads of this merger
-    constexpr int NO = (GT * D_HEAD + DEC_THREADS - 1) / DEC_THREADS;   // outputs per thread (bound)
-    constexpr int OB = NO < 2 ? NO : 2;                                  // outputs per pass (registers)
-    const uint32_t all = M >= 32 ? 0xffffffffu : (1u << M) - 1u;
-    float v[OB][DEC_MAX_RANKS];
-    auto poll_pass = [&](int ob) {
-      uint32_t pend[OB];
+    const int npair = M * nh;                                         // <= DEC_MAX_RANKS
+    float* pbuf = reinterpret_cast<float*>(smem + L.ring);            // [npair][PS] (the ring is free)
+    float* wts = pbuf + DEC_MAX_RANKS * PS;                           // [DEC_MAX_RANKS][GT]
+    float* linv = wts + DEC_MAX_RANKS * GT;                           // [GT]
+    constexpr int PPW = (DEC_MAX_RANKS + DEC_WARPS - 1) / DEC_WARPS;  // pairs per warp
+    constexpr int CPL = (D_HEAD + 2 + 31) / 32;                       // words per lane per pair
+    uint32_t pend = 0u;
 #pragma unroll
-      for (int q = 0; q < OB; ++q) {
-        const int o = tid + (ob + q) * DEC_THREADS;
-        pend[q] = (ob + q < NO && o < nh * D_HEAD) ? all : 0u;
-      }
-      for (unsigned spins = 0;;) {
-        uint32_t any = 0u;
+    for (int a = 0; a < PPW; ++a)
 #pragma unroll
-        for (int q = 0; q < OB; ++q) any |= pend[q];
-        if (!any) break;
-        if (++spins > HATA_SPIN_LIMIT) __trap();
+      for (int c = 0; c < CPL; ++c)
+        if (warp + a * DEC_WARPS < npair && lane + 32 * c < PS) pend |= 1u << (a * CPL + c);
+    const uint64_t* src[PPW];
 #pragma unroll
-        for (int q = 0; q < OB; ++q) {
-          const int o = tid + (ob + q) * DEC_THREADS, h = r + nmerge * (o / D_HEAD), e = o % D_HEAD;
-          uint64_t x[DEC_MAX_RANKS];
+    for (int a = 0; a < PPW; ++a) {
+      const int pr = warp + a * DEC_WARPS, i = pr / nh, hi = pr - i * nh;
+      src[a] = part + i * PB + (r + nmerge * hi) * PS + lane;
+    }
+    for (unsigned spins = 0; pend;) {
+      uint64_t x[PPW * CPL];
 #pragma unroll
-          for (int i = 0; i < DEC_MAX_RANKS; ++i)
-            if ((pend[q] >> i) & 1u) x[i] = ld_relaxed_u64(part + i * PB + h * PS + 2 + e);
+      for (int a = 0; a < PPW; ++a)
 #pragma unroll
-          for (int i = 0; i < DEC_MAX_RANKS; ++i)
-            if (((pend[q] >> i) & 1u) && tag_of(x[i]) == tag) {
-              v[q][i] = __uint_as_float((uint32_t)x[i]);
-              pend[q] &= ~(1u << i);
-            }
-        }
-      }
-    };
+        for (int c = 0; c < CPL; ++c)
+          if ((pend >> (a * CPL + c)) & 1u) x[a * CPL + c] = ld_relaxed_u64(src[a] + 32 * c);
+#pragma unroll
+      for (int a = 0; a < PPW; ++a)
+#pragma unroll
+        for (int c = 0; c < CPL; ++c)
+          if (((pend >> (a * CPL + c)) & 1u) && tag_of(x[a * CPL + c]) == tag) {
+            pbuf[(warp + a * DEC_WARPS) * PS + lane + 32 * c] = __uint_as_float((uint32_t)x[a * CPL + c]);
+            pend &= ~(1u << (a * CPL + c));
+          }
+      if (pend && ++spins > HATA_SPIN_LIMIT) __trap();
+    }
+    HATA_TRACE(12);
+    __syncthreads();
+    HATA_TRACE(14);
     if (warp < nh) {
-      // rank `lane`'s (m, l) of head h
-      const int h = r + nmerge * warp;
-      float mr = -INFINITY, lr = 0.f;
-      if (lane < M)
-        for (unsigned spins = 0;;) {
-          const uint64_t xm = ld_relaxed_u64(part + lane * PB + h * PS), xl = ld_relaxed_u64(part + lane * PB + h * PS + 1);
-          if (tag_of(xm) == tag && tag_of(xl) == tag) { mr = __uint_as_float((uint32_t)xm); lr = __uint_as_float((uint32_t)xl); break; }
-          if (++spins > HATA_SPIN_LIMIT) __trap();
-        }
+      const float mr = lane < M ? pbuf[(lane * nh + warp) * PS] : -INFINITY;
+      const float lr = lane < M ? pbuf[(lane * nh + warp) * PS + 1] : 0.f;
       float Mx = mr;
 #pragma unroll
       for (int x = 16; x > 0; x >>= 1) Mx = fmaxf(Mx, __shfl_xor_sync(0xffffffffu, Mx, x));
@@ -1091,22 +1095,13 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
       if (lane < DEC_MAX_RANKS) wts[lane * GT + warp] = w;
       if (lane == 0) linv[warp] = Ls > 0.f ? 1.f / Ls : 0.f;
     }
-    poll_pass(0);
     __syncthreads();
-    HATA_TRACE(14);
-    for (int ob = 0; ob < NO; ob += OB) {
-      if (ob) poll_pass(ob);
-#pragma unroll
-      for (int q = 0; q < OB; ++q) {
-        const int o = tid + (ob + q) * DEC_THREADS, hi = o / D_HEAD, e = o % D_HEAD;
-        if (ob + q < NO && o < nh * D_HEAD) {
-          float a0 = 0.f;
-#pragma unroll
-          for (int i = 0; i < DEC_MAX_RANKS; ++i)
-            if (i < M) a0 = fmaf(v[q][i], wts[i * GT + hi], a0);       // rank order
-          store_out(r + nmerge * hi, e, a0 * linv[hi]);
-        }
-      }
+    for (int o = tid; o < nh * D_HEAD; o += DEC_THREADS) {
+      const int hi = o / D_HEAD, e = o % D_HEAD;
+      float a0 = 0.f;
+#pragma unroll 6
+      for (int i = 0; i < M; ++i) a0 = fmaf(pbuf[(i * nh + hi) * PS + 2 + e], wts[i * GT + hi], a0);   // rank order
+      store_out(r + nmerge * hi, e, a0 * linv[hi]);
     }
   } else {
     // candidates only: rank 0 has polled every rank's prefix counts (the

@@ -17,9 +17,9 @@ import torch  # noqa: E402
 import bench  # noqa: E402
 import synth  # noqa: E402
 
-NAMES = {31: "kernel_entry", 0: "start", 1: "hash_done", 2: "score_done", 3: "hist_x", 4: "D_staged", 5: "select_done",
+NAMES = {31: "kernel_entry", 0: "start", 1: "hash_done", 2: "score_done", 3: "hist_x", 4: "merge_ml_polled", 5: "select_done",
          6: "attn_done", 7: "end(last)", 8: "qk_loaded", 9: "W_ready", 10: "stage0", 11: "thr",
-         12: "quota", 13: "last_stage", 14: "merge_polled", 15: "published", 16: "kv_gathered",
+         12: "merge_out_polled", 13: "last_stage", 14: "merge_polled", 15: "published", 16: "kv_gathered",
          17: "groups_done", 19: "kv_issued", 20: "kv_gathered_1st", 21: "groups_done_1st",
          23: "kv_issued_1st", 20: "attn_entry", 27: "arrived", 28: "wait_done", 18: "sel_counted", 21: "sel_scanned", 22: "sel_emitted", 29: "attn_wmerge1", 30: "attn_wmerge2", 24: "hash_mma_done(t0)", 25: "hash_synced", 26: "planes_done(t0)"}
 
@@ -36,7 +36,7 @@ def chain(cfg, S=8):
     H = sets[0].H
     M = H.decode_ranks(sh.B, sh.Hq, sh.Hkv, sh.d, sh.rbits, sh.N, sh.k, sets[0].K.dtype)
     nct = M * sh.B * sh.Hkv
-    bufs = [torch.zeros(nct * 64, dtype=torch.int64, device=dev) for _ in range(S)]
+    bufs = [torch.zeros(nct * 96, dtype=torch.int64, device=dev) for _ in range(S)]
 
     def run_all():
         for s, b in zip(sets, bufs):
@@ -51,7 +51,7 @@ def chain(cfg, S=8):
         b.zero_()
     g.replay()
     torch.cuda.synchronize()
-    ts = [b.view(nct, 64).cpu().double() for b in bufs]
+    ts = [b.view(nct, 96).cpu().double() for b in bufs]
     print(f"{cfg} chained x{S}: M={M} ranks x {sh.B * sh.Hkv} units = {nct} CTAs")
     for i in range(1, S):
         prev_end = ts[i - 1][:, 7].max()
@@ -66,6 +66,34 @@ def chain(cfg, S=8):
         cols.sort()
         step = (t[:, 7].max() - prev_end) / 1e3
         print(f"launch{i} step={step.item():.2f}us " + " ".join(f"{nm}={md:.2f}/{mx:.2f}" for md, mx, nm in cols))
+        if i == S - 1:
+            # clock-refined timeline: each stamp = the CTA's wait_done (globaltimer,
+            # 256 ns ticks) + (clock64 delta) / (its own clock rate over the launch)
+            ck = t[:, 64:96]
+            ok = (t[:, 28] > 0) & (t[:, 31] > 0)
+            span_gt = t[:, 15].where(t[:, 15] > 0, t[:, 7]) - t[:, 31]
+            span_ck = ck[:, 15].where(t[:, 15] > 0, ck[:, 7]) - ck[:, 31]
+            f = (span_ck / span_gt.clamp(min=1)).median().item()       # cycles per ns
+            fine = []
+            for j in range(32):
+                sel = ok & (t[:, j] > 0)
+                if sel.any():
+                    v = ((t[sel, 28] - prev_end) + (ck[sel, j] - ck[sel, 28]) / f) / 1e3
+                    fine.append((v.median().item(), v.max().item(), NAMES.get(j, str(j))))
+            fine.sort()
+            print(f"  clock-refined ({f:.3f} GHz): " + " ".join(f"{nm}={md:.2f}/{mx:.2f}" for md, mx, nm in fine))
+            # per rank (median over the units): when it reached each phase, and its selected rows
+            rk = torch.arange(nct) % M
+            for rr in range(M):
+                sel = rk == rr
+                row = []
+                for j in (27, 3, 11, 22, 19, 16, 17, 6, 15, 4, 12, 14, 7):
+                    c = t[sel, j]
+                    c = c[c > 0]
+                    if len(c):
+                        row.append(f"{NAMES.get(j, j)}={((c - prev_end) / 1e3).median().item():.2f}")
+                rows_sel = t[sel, 32 + 15]
+                print(f"  rank{rr:2d} rows={rows_sel.median().item():.0f}/{rows_sel.max().item():.0f} " + " ".join(row))
 
 
 def main():
@@ -81,7 +109,7 @@ def main():
     H = sets[0].H
     M = H.decode_ranks(sh.B, sh.Hq, sh.Hkv, sh.d, sh.rbits, sh.N, sh.k, sets[0].K.dtype)
     nct = M * sh.B * sh.Hkv
-    buf = torch.zeros(nct * 64, dtype=torch.int64, device=dev)
+    buf = torch.zeros(nct * 96, dtype=torch.int64, device=dev)
     for s in sets:
         s.run()
     torch.cuda.synchronize()
@@ -96,7 +124,7 @@ def main():
         (s.run if fused else s.decode)()
         H.lib().hata_debug_timestamp(marks.data_ptr() + 8, st)        # decode kernel done
         torch.cuda.synchronize()
-        t = buf.view(nct, 64).cpu().double()
+        t = buf.view(nct, 96).cpu().double()
         mk = marks.cpu().double()
         t0 = mk[0]
         print(f"rep{rep} marker_before=0  decode_done_marker={(mk[1] - t0).item() / 1e3:.2f} us")
