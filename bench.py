@@ -206,7 +206,7 @@ class Step:
 
     def hint_counters(self):
         """Per-unit (hinted selections, window-exchange thresholds): workspace word 3, 16-bit wrapping."""
-        w = self.ws[:16 * self.sh.B * self.sh.Hkv].view(torch.int32).view(-1, 4)[:, 3].cpu().long() & 0xFFFFFFFF
+        w = self.ws[:32 * self.sh.B * self.sh.Hkv].view(torch.int32).view(-1, 8)[:, 3].cpu().long() & 0xFFFFFFFF
         return (w & 0xFFFF), (w >> 16)
 
 

@@ -136,7 +136,7 @@ DecodePlan plan_decode(int B, int Hq, int Hkv, int d, int rbits, int64_t n_max, 
   // n_max (hence M) and k change; the sections after it are fully written
   // before they are read in a launch.
   size_t off = 0;
-  pl.ws_sync = off;  off += up256((size_t)units * 4 * 4);          // epoch, hint slots (any M)
+  pl.ws_sync = off;  off += up256((size_t)units * DEC_SYNC_WORDS * 4);   // epoch, hint / appended-row slots (any M)
   pl.ws_hist = off;  off += M > 1 ? up256((size_t)units * M * hs * 8) : 0;          // tagged words
   pl.ws_part = off;  off += M > 1 ? up256((size_t)units * M * dec_part_stride(GT, d) * 8) : 0;
   pl.ws_D = off;     off += !pl.d_smem ? up256((size_t)units * M * dec_dchunk(pl.chunk) * 2) : 0;

@@ -32,6 +32,7 @@ constexpr int DEC_CHUNK_ALIGN = 64;          // tokens
 constexpr int DEC_BC_WPT = 4;               // candidate-bitmap words per thread (fast selection path)
 constexpr int DEC_HINT_SLACK = 2;           // hint threshold slack (bins)
 constexpr int DEC_WIN = 32;                 // bins [h - 15, h + 16] (h = previous threshold) of every rank's prefix counts
+constexpr int DEC_SYNC_WORDS = 8;            // per-unit sync words in the workspace
 constexpr int DEC_MAX_RANKS = 32;            // M cap (histogram exchange is M x nbins per rank)
 constexpr int DEC_ROW_PAD = 16;              // bytes of padding per staged K/V row (bank spread)
 constexpr int DEC_QS_PAD = 4;                // floats of padding per q row in smem
@@ -85,7 +86,8 @@ struct DecodeParams {
   uint64_t* ws_hist;       // [units, M, hs] exclusive prefix counts cum_r[0..nbins]   (M > 1)
   uint16_t* ws_D;          // [units, M, chunk] D when it does not fit in smem (!d_smem)
   uint64_t* ws_part;       // [units, M, GT, d+2] float bits  (M > 1)
-  unsigned* ws_sync;       // [units, 4]: epoch, threshold hint (2 slots by epoch parity), hint-use counters
+  unsigned* ws_sync;       // [units, 8]: epoch, threshold hint (2 slots by epoch parity), hint-use counters,
+                           //   appended row + 1 (2 slots by epoch parity), 2 spare
   // sequence-shard phase 1 (hata_shard_candidates): stop after the select and
   // emit (D, global index) candidates instead of attending.
   int cand_mode;
@@ -181,12 +183,12 @@ __host__ __device__ inline DecodeSmem decode_smem_layout(const DecodeParams& p, 
   s.D = off; off += p.d_smem ? up(dec_dchunk(p.chunk) * 2) : 0;
   s.bc = off; off += p.d_smem ? up(dec_dchunk(p.chunk) / 8) : 0;   // candidate bitmap (1 bit per token)
   s.qf = off; off += up((GT + 1) * dec_qstride(p.d) * 4);
-  s.qw = off; off += up((GT + 1) * (p.rbits / 32) * 4);
+  s.qw = off; off += up((GT + 2) * (p.rbits / 32) * 4);   // q codes, new key code, reloaded row
   s.qraw = off; off += up((GT + 2) * p.d * eb);   // q rows, new key, new value
   s.planes = off; off += up((64 + 8) * 4);        // P/N planes [2][4][8] + K0 shares [8]
   s.rows = off; off += p.ws_rows ? 0 : up(p.R_cap * 4);
   s.red = off; off += up((DEC_MAX_RANKS * 4 + 64) * 4);
-  s.chref = off; off += up(DEC_MAX_RANKS * DEC_WIN * 4);
+  s.chref = off; off += up((DEC_MAX_RANKS + 1) * DEC_WIN * 4);
   s.misc = off; off += up(128 * 4);   // [0,16) scalars, [16,80) warp counters, [80,104) softmax m/l/corr
   s.qp = off; off += up(DEC_THREADS * (GT + 1) * 4);
   s.total = off;

@@ -118,6 +118,7 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
   int32_t* red = reinterpret_cast<int32_t*>(smem + L.red);
   int32_t* misc = reinterpret_cast<int32_t*>(smem + L.misc);
   int32_t* win = reinterpret_cast<int32_t*>(smem + L.chref);       // [M][DEC_WIN] prefix counts near the hint
+  int32_t* wtot = win + DEC_MAX_RANKS * DEC_WIN;                    // [DEC_WIN] their unit totals
   float* fmisc = reinterpret_cast<float*>(misc);
 
   // Rank chunks [rr*per, (rr+1)*per) are fixed by the host from n_max, so the
@@ -192,6 +193,7 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
   if (warp == 0 && !ptab)                                           // the code chunk, a few large copies
     for (int s = 0; s < NST && s < nstages; ++s) issue_stage(s);
   for (int i = tid; i < p.nbins; i += DEC_THREADS) hist[i] = 0;
+  if (tid < DEC_WIN) wtot[tid] = 0;
   // L2 prefetch of the small inputs read right after the wait (q rows, new
   // key/value rows, n[b], the unit's hint word): a prefetch only moves lines
   // into L2, the point of coherence, so a value the preceding kernel writes
@@ -205,7 +207,7 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
       prefetch_l2_line(reinterpret_cast<const uint8_t*>(src) + (int64_t)u * D_HEAD * EB + (i % kl) * 128);
     } else if (tid == DEC_THREADS - 1) {
       prefetch_l2_line(p.n + b);
-      if (p.ws_sync) prefetch_l2_line(p.ws_sync + 4 * u);
+      if (p.ws_sync) prefetch_l2_line(p.ws_sync + DEC_SYNC_WORDS * u);
     }
   }
   // Programmatic dependent launch: everything above reads only the hash
@@ -229,13 +231,19 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
                              : reinterpret_cast<const T*>(row == G ? p.k_new : p.v_new) + (int64_t)u * D_HEAD;
       dq[i] = __ldcg(reinterpret_cast<const uint4*>(src) + c);
     }
+    HATA_CLK(17);
     if (tid == 0) {
-      // the unit's sync words in one load: epoch E (this launch tags its
-      // exchange and partials with E + 1), the threshold hint of launch E in
-      // slot 1 + (E & 1) (launch E + 1 writes the other slot)
-      const uint4 sw = p.ws_sync ? __ldcg(reinterpret_cast<const uint4*>(p.ws_sync + 4 * u)) : make_uint4(0, 0, 0, 0);
+      // the unit's sync words (two loads in flight): epoch E (this launch
+      // tags its exchange and partials with E + 1); the threshold hint of
+      // launch E in slot 1 + (E & 1) and the row it appended (+1) in slot
+      // 4 + (E & 1) (launch E + 1 writes the other slots)
+      const uint4* sp = reinterpret_cast<const uint4*>(p.ws_sync + DEC_SYNC_WORDS * u);
+      const uint4 sw = p.ws_sync ? __ldcg(sp) : make_uint4(0, 0, 0, 0);
+      const uint4 sw2 = p.ws_sync ? __ldcg(sp + 1) : make_uint4(0, 0, 0, 0);
       misc[12] = (int)(sw.x + 1u);
       misc[14] = (int)((sw.x & 1u) ? sw.z : sw.y);
+      misc[13] = (int)((sw.x & 1u) ? sw2.y : sw2.x);
+      HATA_CLK(18);
     }
     if (warp == 0 && ptab)                                          // paged: the page table is read after the wait
       for (int s = 0; s < NST && s < nstages; ++s) issue_stage(s);
@@ -272,6 +280,14 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
   if (hinted) { const int h = misc[14]; Th = h > 0 ? h + DEC_HINT_SLACK : -1; hw0 = h - (DEC_WIN / 2 - 1); }
   const uint32_t tag = (uint32_t)misc[12];                          // this launch's epoch tag (>= 1)
   const uint64_t tagw = (uint64_t)tag << 32;
+  // The row the previous launch on this workspace appended: that launch
+  // triggered its dependents without a fence, so this launch's code stream
+  // (started before the wait) may hold a stale copy of it -- re-read it now
+  // (after the wait) and rescore it after the scoring pass (include/hata.h)
+  const int64_t prow = (int64_t)misc[13] - 1;
+  const bool reload = prow >= t0 && prow < t0 + Lr && !(append && prow == pos) && prow < p.cap;
+  uint32_t* qrel = qw + (GT + 1) * W;                               // its code words
+  if (reload && warp == DEC_WARPS - 1 && lane < W) qrel[lane] = __ldcg(p.codes + cmap(prow) + lane);
   HATA_TRACE(9);
   if constexpr (EB != 2) {                                          // fp32 paths read q as floats
     for (int i = tid; i < NV * D_HEAD; i += DEC_THREADS) qf[(i / D_HEAD) * QS + i % D_HEAD] = Elem<T>::to_f(qraw[i]);
@@ -314,6 +330,7 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
       qa[ks][2] = gid < NV ? x0[4] : 0u;
       qa[ks][3] = gid + 8 < NV ? x1[4] : 0u;
     }
+    HATA_CLK(19);
     // warp = one 32-bit code word (4 n-tiles, 4 independent MMA chains);
     // each lane sets its 2 sign bits per n-tile, the 4 lanes of a row OR-reduce
     for (int w = warp; w < W; w += DEC_WARPS) {
@@ -328,6 +345,7 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
           ldsm_x2_trans(b0, b1, reinterpret_cast<const uint8_t*>(Ws) + (ks * 16 + (lane & 15)) * WROWB + (4 * w + q) * 16);
           mma_bf16_16816(c[q], qa[ks], b0, b1);
         }
+      HATA_CLK(20);
       uint32_t lo = 0u, hi = 0u;                                    // rows gid / gid + 8, LSB-first (R7)
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
@@ -351,6 +369,7 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
         if (h < G) cnt += (wh >> lane) & 1u;
       }
       word_planes(w, cnt);
+      HATA_CLK(21);
     }
   } else {
     // fp32: thread = (bit, j-slice), all vectors at once (fp32 FMA; slices
@@ -521,6 +540,19 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
     }
   }
   __syncthreads();                                                  // every D / histogram update done
+  if (reload && tid == 0) {
+    // the previous launch's appended row, re-read after the wait
+    uint32_t kc[W];
+#pragma unroll
+    for (int w = 0; w < W; ++w) kc[w] = qrel[w];
+    const int jl = (int)(prow - t0);
+    const uint32_t Dn = group_D(kc);
+    const uint32_t Do = Dloc[jl];
+    hist[Do] -= 1u;
+    hist[Dn] += 1u;
+    Dloc[jl] = (uint16_t)Dn;
+  }
+  __syncthreads();
   if (owner && tid == 0) {
     // the streamed row pos held the stale code: re-score the appended key
     uint32_t kc[W];
@@ -543,9 +575,9 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
       reinterpret_cast<uint4*>(dstrow)[tid % CH] = v;
       asm volatile("fence.proxy.async.global;" ::: "memory");        // this rank's own gather reads it by TMA
     }
-    // the appended code row and K/V rows are visible GPU-wide before this
-    // CTA triggers its dependents (their code streams start before their wait)
-    __threadfence();
+    // no fence before the trigger: the next launch re-reads this row after
+    // its wait (slot 4 + ((E + 1) & 1) records it)
+    if (tid == 0 && p.ws_sync) p.ws_sync[DEC_SYNC_WORDS * u + 4 + (tag & 1u)] = (unsigned)(pos + 1);
   }
   // pad D past the valid tokens with 0x7fff (never selected) up to what the
   // selection reads: the per-thread blocking (dec_dchunk(Lr)) of the full
@@ -587,6 +619,7 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
     // threshold loop below writes them without a further barrier)
     if (tid == 0) { misc[0] = -1; misc[1] = 0; misc[4] = p.nbins; }
     cum = block_excl_scan(mysum, misc + 16, total);                  // #{local D < i0}
+    HATA_CLK(22);
   }
   auto build_bitmap = [&]() {
     if (Th < 0) return;
@@ -620,6 +653,7 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
       if (q < BPT && i <= p.nbins) st_relaxed_u64(gc + i, tagw | (uint32_t)c);
       c += tb[q];
     }
+    HATA_CLK(24);
     build_bitmap();
     HATA_TRACE(27);
     // the owner's K/V row (generic stores) -> this CTA's gather (async proxy)
@@ -653,6 +687,7 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
         for (int j = 0; j < WJ; ++j)
           if (((pend >> j) & 1u) && tag_of(x[j]) == tag) {
             win[tid + j * DEC_THREADS] = (int)(uint32_t)x[j];
+            atomicAdd(&wtot[(tid + j * DEC_THREADS) % DEC_WIN], (int)(uint32_t)x[j]);
             pend &= ~(1u << j);
           }
         if (pend && ++spins > HATA_SPIN_LIMIT) __trap();           // a lost rank: fail loudly, never hang
@@ -662,11 +697,7 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
     HATA_TRACE(3);
     static_assert(DEC_WIN == 32, "one lane per window bin");
     if (warp == 0) {
-      int tot = 0;
-      if (Th >= 0) {
-#pragma unroll 8
-        for (int rr = 0; rr < M; ++rr) tot += win[rr * DEC_WIN + lane];
-      }
+      const int tot = Th >= 0 ? wtot[lane] : 0;                       // unit total at bin w0 + lane
       const int z = __shfl_down_sync(0xffffffffu, tot, 1);
       const int bj = w0 + lane;                                       // bins bj, bj + 1 both in the window
       const bool hit = Th >= 0 && lane < DEC_WIN - 1 && bj >= 0 && bj + 1 <= p.nbins && kp > 0 && tot < kp && kp <= z;
@@ -717,7 +748,7 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
   __syncthreads();
   const int thr = misc[0];
   const int need = misc[1];
-  if (p.ws_sync && r == 0 && tid == 0) reinterpret_cast<int*>(p.ws_sync)[4 * u + 1 + (tag & 1u)] = thr;   // launch E+1's hint slot
+  if (p.ws_sync && r == 0 && tid == 0) reinterpret_cast<int*>(p.ws_sync)[DEC_SYNC_WORDS * u + 1 + (tag & 1u)] = thr;   // launch E+1's hint slot
   // this rank's tie quota and the selection position of its first token
   // (computed by every warp: no further barrier); the loads are issued here
   // and consumed after the counting pass below
@@ -800,8 +831,8 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
     // diagnostics word: launches whose selection took the
     // hinted path (low 16 bits) and whose threshold came from the window
     // exchange (high 16 bits), per unit, wrapping
-    unsigned* cnt = p.ws_sync + 4 * u + 3;
-    *cnt += (fast ? 1u : 0u) + ((M > 1 && misc[5]) ? 0x10000u : 0u);
+    unsigned* cnt = p.ws_sync + DEC_SYNC_WORDS * u + 3;
+    atomicAdd(cnt, (fast ? 1u : 0u) + ((M > 1 && misc[5]) ? 0x10000u : 0u));   // no return: not on the critical path
   }
   if (fast) {
     const int WPT = (nbw + DEC_THREADS - 1) / DEC_THREADS;
@@ -832,9 +863,12 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
         nlt += __popc(lt);
         neq += __popc(eq);
       }
+      HATA_CLK(25);
       int ti_b, lt_tot, ti_tot;
       int lt_b = block_excl_scan2(nlt, neq, misc + 16, ti_b, lt_tot, ti_tot);
+      HATA_CLK(26);
       compute_quota();
+      HATA_CLK(27);
       Rr = lt_tot + min(ti_tot, quota);
 #pragma unroll
       for (int j = 0; j < WPTC; ++j) {
@@ -1000,7 +1034,7 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
         }
       }
     }
-    if (p.ws_sync && tid == 0) p.ws_sync[4 * u] = tag;              // advance the unit's epoch
+    if (p.ws_sync && tid == 0) p.ws_sync[DEC_SYNC_WORDS * u] = tag;              // advance the unit's epoch
     HATA_TRACE(7);
     return;
   }
@@ -1096,6 +1130,7 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
       if (lane == 0) linv[warp] = Ls > 0.f ? 1.f / Ls : 0.f;
     }
     __syncthreads();
+    HATA_CLK(29);
     for (int o = tid; o < nh * D_HEAD; o += DEC_THREADS) {
       const int hi = o / D_HEAD, e = o % D_HEAD;
       float a0 = 0.f;
@@ -1103,6 +1138,7 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
       for (int i = 0; i < M; ++i) a0 = fmaf(pbuf[(i * nh + hi) * PS + 2 + e], wts[i * GT + hi], a0);   // rank order
       store_out(r + nmerge * hi, e, a0 * linv[hi]);
     }
+    HATA_CLK(30);
   } else {
     // candidates only: rank 0 has polled every rank's prefix counts (the
     // exchange) before it advances the epoch below
@@ -1111,7 +1147,7 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
   // advance the unit's epoch: rank 0 has seen a tagged word of every rank
   // (its partials, or in candidates mode the exchange), so every CTA of this
   // launch has read the old epoch
-  if (r == 0 && tid == 0) p.ws_sync[4 * u] = tag;
+  if (r == 0 && tid == 0) p.ws_sync[DEC_SYNC_WORDS * u] = tag;
   HATA_TRACE(7);
   HATA_CLK(14);
 }

@@ -80,8 +80,18 @@ def chain(cfg, S=8):
                 if sel.any():
                     v = ((t[sel, 28] - prev_end) + (ck[sel, j] - ck[sel, 28]) / f) / 1e3
                     fine.append((v.median().item(), v.max().item(), NAMES.get(j, str(j))))
+            CLKN = {17: "q_rows_loaded(t0)", 18: "sync_words_loaded", 19: "hash_qa_loaded", 20: "hash_mma_chain_done",
+                    21: "hash_planes_w0", 22: "prefix_scanned", 24: "counts_published", 25: "fsel_words_done",
+                    26: "fsel_scanned", 27: "fsel_quota", 29: "merge_weights_synced", 30: "merge_outputs_done"}
+            for j, nm in CLKN.items():
+                sel = ok & (t[:, 32 + j] > 0)
+                if sel.any():
+                    v = ((t[sel, 28] - prev_end) + (t[sel, 32 + j] - ck[sel, 28]) / f) / 1e3
+                    fine.append((v.median().item(), v.max().item(), "c:" + nm))
             fine.sort()
-            print(f"  clock-refined ({f:.3f} GHz): " + " ".join(f"{nm}={md:.2f}/{mx:.2f}" for md, mx, nm in fine))
+            print(f"  clock-refined ({f:.3f} GHz):")
+            for md, mx, nm in fine:
+                print(f"    {md:7.2f} {mx:7.2f}  {nm}")
             # per rank (median over the units): when it reached each phase, and its selected rows
             rk = torch.arange(nct) % M
             for rr in range(M):
@@ -93,7 +103,11 @@ def chain(cfg, S=8):
                     if len(c):
                         row.append(f"{NAMES.get(j, j)}={((c - prev_end) / 1e3).median().item():.2f}")
                 rows_sel = t[sel, 32 + 15]
-                print(f"  rank{rr:2d} rows={rows_sel.median().item():.0f}/{rows_sel.max().item():.0f} " + " ".join(row))
+                sp = t[sel, 32 + 16]
+                used = (sp >= 100000).double().mean().item()
+                cands = sp % 100000
+                print(f"  rank{rr:2d} rows={rows_sel.median().item():.0f}/{rows_sel.max().item():.0f} "
+                      f"spec={cands.median().item():.0f}/{cands.max().item():.0f} used={used:.2f} " + " ".join(row))
 
 
 def main():
