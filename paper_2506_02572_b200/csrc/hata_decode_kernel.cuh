@@ -511,8 +511,10 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
   if (!recycle) {
     // the whole chunk fits the ring (and was streamed before the wait): one
     // flat pass over it once every stage has landed
-    for (int s = 0; s < nstages; ++s)
+    for (int s = 0; s < nstages; ++s) {
       if (!(HATA_DIAG && (p.dbg & 16))) mbar_wait(&bars[s], 0u);
+      if (s < 3) HATA_CLK(11 + s);
+    }
     HATA_TRACE(10);
     const int copied = nstages ? (nstages - 1) * STAGE_TOK + copied_tok(nstages - 1) : 0;
     const int npairs = max(0, min(Lr, copied)) / 2;
@@ -627,11 +629,15 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
     // words [t*WPT, (t+1)*WPT) (32 tokens each); bit i of word w = (D[32w+i] <= Th)
     const uint32_t th_k = (uint32_t)Th * 0x10001u + 0x80008000u;
     const int WPT = (nbw + DEC_THREADS - 1) / DEC_THREADS;
+    // the 16-byte quarters of a word are read in a per-thread rotated order:
+    // 8 consecutive threads then touch 8 distinct bank groups (WPT odd)
+    const int rot = (WPT & 1) ? (tid >> 1) : tid;
     for (int w = tid * WPT; w < min(nbw, (tid + 1) * WPT); ++w) {
       const uint4* dq = reinterpret_cast<const uint4*>(Dloc + 32 * w);
       uint32_t m = 0u;
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
+      for (int c0 = 0; c0 < 4; ++c0) {
+        const int c = (c0 + rot) & 3;
         const uint4 x = dq[c];
         const uint32_t a0 = (th_k - x.x) & 0x80008000u, a1 = (th_k - x.y) & 0x80008000u;
         const uint32_t a2 = (th_k - x.z) & 0x80008000u, a3 = (th_k - x.w) & 0x80008000u;
@@ -849,8 +855,10 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
         if (j < WPT && w < nbw && Bc[w]) {
           // the word's 32 distances by SWAR (bounded cost for dense words)
           const uint4* dq = reinterpret_cast<const uint4*>(Dloc + 32 * w);
+          const int rot = (WPT & 1) ? (tid >> 1) : tid;               // conflict-free quarter order
 #pragma unroll
-          for (int c = 0; c < 4; ++c) {
+          for (int c0 = 0; c0 < 4; ++c0) {
+            const int c = (c0 + rot) & 3;
             const uint4 x = dq[c];
             uint32_t l4[4], e4[4];
             swar(x.x, l4[0], e4[0]); swar(x.y, l4[1], e4[1]); swar(x.z, l4[2], e4[2]); swar(x.w, l4[3], e4[3]);
@@ -892,8 +900,10 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
   } else {
     int lt_m = 0, eq_m = 0;
     if (thr >= 0) {
+      const int rot = tid >> 1;                                       // conflict-free block order (counts only)
   #pragma unroll 4
-      for (int c = 0; c < S8; ++c) {
+      for (int c0 = 0; c0 < S8; ++c0) {
+        const int c = (c0 + rot) % S8;
         const uint4 x = Dv[c];
         uint32_t l0, e0, l1, e1, l2, e2, l3, e3;
         swar(x.x, l0, e0); swar(x.y, l1, e1); swar(x.z, l2, e2); swar(x.w, l3, e3);
@@ -1080,8 +1090,6 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
     const int nh = (G - r + nmerge - 1) / nmerge;                     // heads of this merger
     const int npair = M * nh;                                         // <= DEC_MAX_RANKS
     float* pbuf = reinterpret_cast<float*>(smem + L.ring);            // [npair][PS] (the ring is free)
-    float* wts = pbuf + DEC_MAX_RANKS * PS;                           // [DEC_MAX_RANKS][GT]
-    float* linv = wts + DEC_MAX_RANKS * GT;                           // [GT]
     constexpr int PPW = (DEC_MAX_RANKS + DEC_WARPS - 1) / DEC_WARPS;  // pairs per warp
     constexpr int CPL = (D_HEAD + 2 + 31) / 32;                       // words per lane per pair
     uint32_t pend = 0u;
@@ -1116,9 +1124,12 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
     HATA_TRACE(12);
     __syncthreads();
     HATA_TRACE(14);
-    if (warp < nh) {
-      const float mr = lane < M ? pbuf[(lane * nh + warp) * PS] : -INFINITY;
-      const float lr = lane < M ? pbuf[(lane * nh + warp) * PS + 1] : 0.f;
+    // warp = 32 outputs of one head hi: lane i holds rank i's merge weight
+    // e^{m_i - M_h} (shuffled into the rank-ordered sum), no smem round trip
+    for (int o0 = warp * 32; o0 < nh * D_HEAD; o0 += DEC_THREADS) {
+      const int hi = o0 / D_HEAD, e = o0 % D_HEAD + lane;
+      const float mr = lane < M ? pbuf[(lane * nh + hi) * PS] : -INFINITY;
+      const float lr = lane < M ? pbuf[(lane * nh + hi) * PS + 1] : 0.f;
       float Mx = mr;
 #pragma unroll
       for (int x = 16; x > 0; x >>= 1) Mx = fmaxf(Mx, __shfl_xor_sync(0xffffffffu, Mx, x));
@@ -1126,17 +1137,11 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
       float Ls = lr * w;
 #pragma unroll
       for (int x = 16; x > 0; x >>= 1) Ls += __shfl_xor_sync(0xffffffffu, Ls, x);
-      if (lane < DEC_MAX_RANKS) wts[lane * GT + warp] = w;
-      if (lane == 0) linv[warp] = Ls > 0.f ? 1.f / Ls : 0.f;
-    }
-    __syncthreads();
-    HATA_CLK(29);
-    for (int o = tid; o < nh * D_HEAD; o += DEC_THREADS) {
-      const int hi = o / D_HEAD, e = o % D_HEAD;
+      HATA_CLK(29);
       float a0 = 0.f;
 #pragma unroll 6
-      for (int i = 0; i < M; ++i) a0 = fmaf(pbuf[(i * nh + hi) * PS + 2 + e], wts[i * GT + hi], a0);   // rank order
-      store_out(r + nmerge * hi, e, a0 * linv[hi]);
+      for (int i = 0; i < M; ++i) a0 = fmaf(pbuf[(i * nh + hi) * PS + 2 + e], __shfl_sync(0xffffffffu, w, i), a0);   // rank order
+      store_out(r + nmerge * hi, e, a0 * (Ls > 0.f ? 1.f / Ls : 0.f));
     }
     HATA_CLK(30);
   } else {

@@ -82,7 +82,8 @@ def chain(cfg, S=8):
                     fine.append((v.median().item(), v.max().item(), NAMES.get(j, str(j))))
             CLKN = {17: "q_rows_loaded(t0)", 18: "sync_words_loaded", 19: "hash_qa_loaded", 20: "hash_mma_chain_done",
                     21: "hash_planes_w0", 22: "prefix_scanned", 24: "counts_published", 25: "fsel_words_done",
-                    26: "fsel_scanned", 27: "fsel_quota", 29: "merge_weights_synced", 30: "merge_outputs_done"}
+                    26: "fsel_scanned", 27: "fsel_quota", 29: "merge_weights(t0)", 30: "merge_outputs_done",
+                    11: "stage0_landed", 12: "stage1_landed", 13: "stage2_landed"}
             for j, nm in CLKN.items():
                 sel = ok & (t[:, 32 + j] > 0)
                 if sel.any():
