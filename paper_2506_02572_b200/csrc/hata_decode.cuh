@@ -30,7 +30,10 @@ constexpr int DEC_MAX_STAGES = 4;            // code ring depth (up to 128 KB in
 constexpr int DEC_D_SMEM_MAX = 16384;        // tokens/CTA whose D (u16) stays in smem
 constexpr int DEC_CHUNK_ALIGN = 64;          // tokens
 constexpr int DEC_BC_WPT = 4;               // candidate-bitmap words per thread (fast selection path)
-constexpr int DEC_HINT_SLACK = 2;           // hint threshold slack (bins)
+#ifndef HATA_HINT_SLACK
+#define HATA_HINT_SLACK 6   // measured: 2 -> 77 % hinted selections, 6 -> 98 % (-0.2 us/step)
+#endif
+constexpr int DEC_HINT_SLACK = HATA_HINT_SLACK;   // hint threshold slack (bins)
 constexpr int DEC_WIN = 32;                 // bins [h - 15, h + 16] (h = previous threshold) of every rank's prefix counts
 constexpr int DEC_SYNC_WORDS = 8;            // per-unit sync words in the workspace
 constexpr int DEC_MAX_RANKS = 32;            // M cap (histogram exchange is M x nbins per rank)

@@ -232,7 +232,7 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
       dq[i] = __ldcg(reinterpret_cast<const uint4*>(src) + c);
     }
     HATA_CLK(17);
-    if (tid == 0) {
+    if (tid == DEC_THREADS - 1) {                                    // (not one of the q-row threads)
       // the unit's sync words (two loads in flight): epoch E (this launch
       // tags its exchange and partials with E + 1); the threshold hint of
       // launch E in slot 1 + (E & 1) and the row it appended (+1) in slot
