@@ -153,9 +153,14 @@ hata_status hata_append(const void* k_new, const void* v_new, hata_dtype dt, con
  *   out_score  optional [B, H_kv, k] int32: S = G*rbits - 2D of those tokens.
  *   out_qcodes optional [B, H_q, rbits/32] uint32: the query codes used.
  *   workspace  device scratch of >= hata_decode_workspace_size(...) bytes,
- *              256-byte aligned, ZERO-FILLED before its first use (every
- *              launch leaves its synchronisation words zeroed again); one
- *              workspace per concurrently running call.  A workspace is tied
+ *              256-byte aligned, ZERO-FILLED before its first use; one
+ *              workspace per concurrently running call.  Per (b, KV head) it
+ *              carries 8 words between launches: an epoch (each launch tags
+ *              the words its CTAs exchange -- prefix counts, softmax
+ *              partials -- with epoch + 1, so readers poll for that tag and
+ *              no word is ever reset), and, in two slots chosen by epoch
+ *              parity, the last selection threshold and the row the last
+ *              fused step appended.  A workspace is tied
  *              to (B, H_kv, G*rbits): launches on it may change n_max and k
  *              (its size must cover the largest), not those three.  It also keeps each
  *              (b, KV head)'s last selection threshold, a hint that lets the
@@ -169,9 +174,13 @@ hata_status hata_append(const void* k_new, const void* v_new, hata_dtype dt, con
  * (q, k_new, v_new, n, K/V, workspace) after it.  Contract: a kernel that
  * precedes this launch in the stream and writes code rows must make those
  * writes visible (__threadfence) before it triggers programmatic completion;
- * every libhata kernel does (fence, then griddepcontrol.launch_dependents),
- * and a kernel that never triggers is complete before this one starts.  The
- * row a fused decode step appends itself is rescored from its own k_new.
+ * hata_hash_keys, hata_prefill_write and hata_append do (fence, then
+ * griddepcontrol.launch_dependents), and a kernel that never triggers is
+ * complete before this one starts.  The decode kernels themselves trigger
+ * without a fence: each records the row it appends in the workspace, and
+ * the next decode launch on that workspace re-reads that row after its
+ * wait and rescores it (so keep one workspace per cache).  The row a fused
+ * decode step appends itself is rescored from its own k_new.
  * One kernel launch of M x (B*H_kv) CTAs (hata_decode_ranks()), at most one
  * per SM; cooperative when HATA_OPT_COOPERATIVE is set.
  * Errors: INVALID_ARG (k < 1, H_q % H_kv, rbits % 32, n_max < 0, nulls),
