@@ -83,7 +83,10 @@ __device__ __forceinline__ int block_excl_scan2(int a, int b, int* buf, int& eb,
 
 template <typename T, int W, int GT, int D_HEAD>
 __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __grid_constant__ DecodeParams p) {
-  constexpr int J = sw_planes_for_group(GT);                       // signed-weight planes
+  // signed-weight planes; the G = 5 template uses the odd-G form (two planes
+  // of t_b = (G-1)/2 - c_b plus the key's own bits, hata_score.cuh)
+  constexpr bool ODDG = GT == 5;
+  constexpr int J = ODDG ? 2 : sw_planes_for_group(GT);
   constexpr int STAGE_TOK = DEC_STAGE_BYTES / (W * 4);
   constexpr int EB = sizeof(T);
   constexpr int NSL = AttnState<GT, D_HEAD>::NSL;
@@ -299,7 +302,7 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
   // share of the constant K0 go to smem (whole warp)
   const int sgn_s = (G % 2 == 0) ? 1 : 0;
   auto word_planes = [&](int w, int c) {
-    const int v = (G - 2 * c) >> sgn_s;                              // exact: G - 2c is even for even G
+    const int v = ODDG ? ((G - 1) >> 1) - c : (G - 2 * c) >> sgn_s;  // exact: G - 2c is even for even G
     const int mag = v < 0 ? -v : v;
     int negc = 0;
 #pragma unroll
@@ -310,7 +313,7 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
       if (lane == 0) { planes[j * 8 + w] = pj; planes[32 + j * 8 + w] = nj; }
     }
     const int csum = warp_sum_i(c);
-    if (lane == 0) reinterpret_cast<int*>(planes)[64 + w] = csum - (negc << sgn_s);   // K0 share of this word
+    if (lane == 0) reinterpret_cast<int*>(planes)[64 + w] = csum - (negc << (ODDG ? 1 : sgn_s));   // K0 share of this word
   };
   if constexpr (EB == 2) {
     // bf16: the projection X[NV x d] . W_g[d x rbits] on the tensor cores
@@ -438,7 +441,8 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
 #pragma unroll
   for (int w = 0; w < W; ++w) K0 += reinterpret_cast<const int*>(planes)[64 + w];
   auto group_D = [&](const uint32_t (&kc)[W]) -> uint32_t {        // D = K0 + (T << s)
-    return (uint32_t)(K0 + (int)(group_distance_sw<W, J>(kc, A, Bp) << sgn_s));
+    if constexpr (ODDG) return (uint32_t)(K0 + (int)group_distance_odd<W>(kc, A, Bp));
+    else return (uint32_t)(K0 + (int)(group_distance_sw<W, J>(kc, A, Bp) << sgn_s));
   };
 
   HATA_TRACE(1);
