@@ -4,13 +4,14 @@
 //
 // Work decomposition: a "unit" is one (b, KV head);
 // each unit is served by M CTAs ("ranks") that own contiguous token chunks, so
-// the grid (M x units) covers the 148 SMs even when B*H_kv is small.  The
-// launch is cooperative (all CTAs co-resident) and the ranks of a unit meet
-// exactly once, at a global-memory barrier after scoring, to exchange their
-// D-histogram prefix counts.  Every rank then derives the same threshold,
-// its own tie quota and output offset, compacts its OWN selected tokens in
-// token order, attends to them, and the last rank to finish merges the M
-// softmax partials in rank order.
+// the grid (M x units) covers the 148 SMs even when B*H_kv is small.  The grid
+// never exceeds one CTA per SM (co-resident once the SMs are free) and the
+// ranks of a unit exchange data twice, through epoch-tagged 64-bit words in
+// the workspace that the readers poll (no fences, no counters): the
+// D-histogram prefix counts after scoring -- every rank then derives the same
+// threshold, its own tie quota and output offset, compacts its OWN selected
+// tokens in token order and attends to them -- and the softmax partials,
+// merged in rank order by min(G, M) merger ranks (one or more heads each).
 //
 // PAPER: Alg. 3 lines 6, 10-17; §4.
 // Readings R1-R20 are listed in DESIGN.md.
@@ -208,12 +209,6 @@ __host__ __device__ inline DecodeSmem decode_smem_layout(const DecodeParams& p, 
   return s;
 }
 
-// ----------------------------------------------------------------- helpers
-__device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
-  unsigned v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
 // 64-bit tagged words of the exchange / merge (single-copy atomic when aligned)
 __device__ __forceinline__ uint64_t ld_relaxed_u64(const uint64_t* p) {
   uint64_t v;
@@ -224,16 +219,6 @@ __device__ __forceinline__ void st_relaxed_u64(uint64_t* p, uint64_t v) {
   asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 __device__ __forceinline__ uint32_t tag_of(uint64_t v) { return (uint32_t)(v >> 32); }
-// Release-add without a return value (arrival at a barrier counter).
-__device__ __forceinline__ void red_add_release_gpu(unsigned* p, unsigned v) {
-  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-// Add with acquire-release semantics, returning the old value.
-__device__ __forceinline__ unsigned atom_add_acq_rel_gpu(unsigned* p, unsigned v) {
-  unsigned old;
-  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
-  return old;
-}
 __device__ __forceinline__ void prefetch_l2_line(const void* g) {
   asm volatile("prefetch.global.L2 [%0];" ::"l"(g) : "memory");
 }
