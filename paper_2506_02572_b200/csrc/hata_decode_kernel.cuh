@@ -243,7 +243,9 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
       const uint4* sp = reinterpret_cast<const uint4*>(p.ws_sync + DEC_SYNC_WORDS * u);
       const uint4 sw = p.ws_sync ? __ldcg(sp) : make_uint4(0, 0, 0, 0);
       const uint4 sw2 = p.ws_sync ? __ldcg(sp + 1) : make_uint4(0, 0, 0, 0);
-      misc[12] = (int)(sw.x + 1u);
+      // tag E + 1; 0 (the zero-filled workspace) is never a tag: after 2^32
+      // launches E + 1 wraps to 2, keeping the epoch parity alternating
+      misc[12] = (int)(sw.x + 1u == 0u ? 2u : sw.x + 1u);
       misc[14] = (int)((sw.x & 1u) ? sw.z : sw.y);
       misc[13] = (int)((sw.x & 1u) ? sw2.y : sw2.x);
       HATA_CLK(18);
