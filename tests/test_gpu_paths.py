@@ -211,3 +211,29 @@ def test_noncontiguous_inputs_equal_contiguous():
         assert torch.equal(st["K"][:, :, sh.N - 1], case["k_new"]) and torch.equal(st["V"][:, :, sh.N - 1], case["v_new"])
         outs.append((o["out"].clone(), o["idx"].clone()))
     assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])
+
+
+def test_epoch_wrap_keeps_results():
+    """The workspace's per-unit epoch (the tag of the exchanged prefix counts
+    and partials) is set just below its 32-bit wrap: the launches that wrap it
+    (tag 0 is skipped: the zero-filled workspace carries tag 0) stay
+    bit-exact in the selection and within tolerance in the output, with the
+    threshold hint carried across the wrap."""
+    sh = _shape("cfg2", N=16384, k=300)
+    case = synth.make_case(sh, seed=37, device="cuda")
+    st = resident_setup(case, case["n_before"])
+    H.append(case["k_new"], case["v_new"], st["W"], st["K"], st["V"], st["codes"], st["nb"])
+    ws, _ = _ws(sh, sh.N, sh.k)
+    n = torch.full((sh.B,), sh.N, dtype=torch.int64, device="cuda")
+    units = sh.B * sh.Hkv
+    for rep in range(4):
+        if rep == 1:
+            words = ws[:32 * units].view(torch.int32).view(units, 8)
+            words[:, 0] = -2                                      # epoch 0xFFFFFFFE: the next launches wrap
+        o = new_outputs(sh, sh.k)
+        H.decode_topk_attn(case["q"], st["K"], st["V"], st["codes"], st["W"], n, sh.k, n_max=sh.N, out=o["out"],
+                           out_idx=o["idx"], out_score=o["score"], out_qcodes=o["qc"], workspace=ws)
+        torch.cuda.synchronize()
+        epochs = ws[:32 * units].view(torch.int32).view(units, 8)[:, 0].cpu().long() & 0xFFFFFFFF
+        print(rep, epochs.tolist()[:2], check_units(case, _res(st, o, n), sh.k, [(0, 0), (0, 3), (0, 7)]))
+    assert (epochs == 3).all()                                    # 0xFFFFFFFE -> 0xFFFFFFFF -> 2 -> 3
