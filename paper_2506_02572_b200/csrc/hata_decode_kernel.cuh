@@ -560,8 +560,7 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) hata_decode_kernel(const __gri
     hist[Dn] += 1u;
     Dloc[jl] = (uint16_t)Dn;
   }
-  __syncthreads();
-  if (owner && tid == 0) {
+  if (owner && tid == 0) {                                          // (same thread: ordered after the reload)
     // the streamed row pos held the stale code: re-score the appended key
     uint32_t kc[W];
 #pragma unroll
