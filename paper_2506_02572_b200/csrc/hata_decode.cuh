@@ -32,7 +32,7 @@ constexpr int DEC_D_SMEM_MAX = 16384;        // tokens/CTA whose D (u16) stays i
 constexpr int DEC_CHUNK_ALIGN = 64;          // tokens
 constexpr int DEC_BC_WPT = 4;               // candidate-bitmap words per thread (fast selection path)
 #ifndef HATA_HINT_SLACK
-#define HATA_HINT_SLACK 6   // measured: 2 -> 77 % hinted selections, 6 -> 98 % (-0.2 us/step)
+#define HATA_HINT_SLACK 10  // measured (CFG-4, q varying): 2 -> 77 % hinted selections, 6 -> 98 %, 10 -> 100 % (17.84 -> 17.45 -> 17.30 us)
 #endif
 constexpr int DEC_HINT_SLACK = HATA_HINT_SLACK;   // hint threshold slack (bins)
 constexpr int DEC_WIN = 32;                 // bins [h - 15, h + 16] (h = previous threshold) of every rank's prefix counts
